@@ -1,0 +1,192 @@
+"""Generate golden vectors by running the UNMODIFIED reference package.
+
+Run in the build container (the reference is at /root/reference, read-only):
+
+    python -B tests/golden/make_golden.py
+
+It imports ``ddccanet`` from /root/reference/pkg/src (matplotlib is stubbed
+because ddccanet.pipeline imports report.py, which imports matplotlib at
+module load; nothing on the fit/transform path draws), runs the reference's
+own functions on seeded inputs, and writes inputs + outputs to
+tests/golden/*.npz. Those fixtures travel with the repo; /root/reference does
+not exist on the GPU box. Inputs are rounded to float32 first because the
+device path stores float32 maps.
+"""
+
+from __future__ import annotations
+
+import sys
+import types
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+
+
+def _import_reference():
+    sys.path.insert(0, str(REF))
+    for name in ("matplotlib", "matplotlib.pyplot"):
+        mod = types.ModuleType(name)
+        mod.use = lambda *a, **k: None
+        sys.modules.setdefault(name, mod)
+    import ddccanet  # noqa: F401
+    import ddccanet.pipeline  # noqa: F401
+    return ddccanet
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def rect_blobs(n, p, q, classes, seed, noise=0.02):
+    """Rectangular generalization of synthetic.make_blob_images (synthetic.py:41-71)."""
+    rng = np.random.default_rng(seed)
+    ang = 2.0 * np.pi * np.arange(classes) / classes + np.pi / 4.0
+    cy0 = p / 2.0 + (p / 4.0) * np.sin(ang)
+    cx0 = q / 2.0 + (q / 4.0) * np.cos(ang)
+    yy, xx = np.mgrid[0:p, 0:q]
+    s = min(p, q)
+    imgs = np.empty((n, p, q))
+    labels = np.arange(n) % classes
+    for k in range(n):
+        c = labels[k]
+        cy, cx = cy0[c] + rng.normal(0, p / 32.0), cx0[c] + rng.normal(0, q / 32.0)
+        amp = rng.uniform(0.75, 1.0)
+        dy, dx = yy - cy, xx - cx
+        if c % 2 == 0:
+            su = sv = (s / 6.0) * rng.uniform(0.9, 1.1)
+            u, v = dy, dx
+        else:
+            su = (s / 4.0) * rng.uniform(0.9, 1.1)
+            sv = (s / 10.0) * rng.uniform(0.9, 1.1)
+            u, v = (dy + dx) / np.sqrt(2.0), (dy - dx) / np.sqrt(2.0)
+        img = np.clip(amp * np.exp(-(u * u) / (2 * su * su) - (v * v) / (2 * sv * sv)), 0, 1)
+        img = np.clip(img + rng.normal(0, noise, (p, q)), 0, 1)
+        imgs[k] = img
+    return imgs, labels
+
+
+def main():
+    dd = _import_reference()
+    from ddccanet.cascade import apply_filters, layer_input
+    from ddccanet.pipeline import compute_features
+    from ddccanet.solver import FilterLayer
+
+    # ---- patches -----------------------------------------------------------
+    rng = np.random.default_rng(11)
+    plane = f32(rng.uniform(size=(7, 9)))
+    geoms = [(3, 3, 1, "zero_same"), (2, 4, 1, "zero_same"), (5, 5, 2, "zero_same"),
+             (1, 1, 1, "zero_same"), (4, 2, 3, "zero_same"), (2, 2, 1, "none"), (4, 6, 1, "zero_same")]
+    rec = {"plane": plane}
+    for k, (l1, l2, s, pad) in enumerate(geoms):
+        g = dd.PatchGeometry(l1, l2, stride=s, padding=pad)
+        rec[f"geom{k}"] = np.array([l1, l2, s, 1 if pad == "zero_same" else 0])
+        rec[f"raw{k}"] = dd.extract_patches(plane, g, center=False).values
+        rec[f"cen{k}"] = dd.extract_patches(plane, g, center=True).values
+    np.savez_compressed(OUT / "patches.npz", **rec)
+
+    # ---- moments -------------------------------------------------------------
+    rng = np.random.default_rng(0)
+    x = f32(rng.standard_normal((6, 40)))
+    y = f32(rng.standard_normal((6, 40)))
+    lab = rng.integers(0, 3, size=40)
+    acc = dd.MomentAccumulator.zeros(6, 3)
+    dd.accumulate_batch(acc, x[:, :17], y[:, :17], lab[:17])
+    dd.accumulate_batch(acc, x[:, 17:], y[:, 17:], lab[17:])
+    fin = dd.finalize(acc, 1e-4)
+    np.savez_compressed(OUT / "moments.npz", x=x, y=y, labels=lab, c11=acc.c11, c22=acc.c22,
+                        s1=acc.class_sum1, s2=acc.class_sum2, g1=acc.global_sum1,
+                        g2=acc.global_sum2, n=acc.patch_count, n_class=acc.per_class_patch_count,
+                        f_c11=fin.c11, f_c22=fin.c22, f_cw=fin.cw, f_cb=fin.cb, f_ct=fin.ctilde)
+
+    # ---- solver --------------------------------------------------------------
+    rng = np.random.default_rng(5)
+    rec = {}
+    for k, dim in enumerate((5, 9, 25, 49)):
+        def spd(n, cond=50.0):
+            qm, _ = np.linalg.qr(rng.standard_normal((n, n)))
+            return (qm * np.geomspace(1.0, cond, n)) @ qm.T
+        c11, c22 = spd(dim), spd(dim)
+        ct = rng.standard_normal((dim, dim))
+        m = dd.DiscriminantMoments(c11=c11, c22=c22, cw=ct, cb=np.zeros_like(ct), ctilde=ct, patch_count=1)
+        count = min(8, dim)
+        pr = dd.solve_dcca(m, count)
+        w, v = dd.sym_eig(0.5 * (c11 + c11.T))
+        rec.update({f"c11_{k}": c11, f"c22_{k}": c22, f"ct_{k}": ct, f"w1_{k}": pr.w1, f"w2_{k}": pr.w2,
+                    f"rho_{k}": pr.rho, f"eigw_{k}": w, f"eigv_{k}": v, f"count_{k}": count})
+    # zero coupling -> null-space completion path
+    qm, _ = np.linalg.qr(rng.standard_normal((4, 4)))
+    c = (qm * np.geomspace(1, 50, 4)) @ qm.T
+    m = dd.DiscriminantMoments(c11=c, c22=c, cw=np.zeros((4, 4)), cb=np.zeros((4, 4)),
+                               ctilde=np.zeros((4, 4)), patch_count=1)
+    pr = dd.solve_dcca(m, 3)
+    rec.update({"zc_c": c, "zc_w1": pr.w1, "zc_w2": pr.w2, "zc_rho": pr.rho})
+    # diagonal case with a degenerate run (exercises _order_degenerate)
+    w, v = dd.sym_eig(np.diag([2.0, 5.0, 2.0, 2.0, 1.0]))
+    rec.update({"deg_w": w, "deg_v": v})
+    np.savez_compressed(OUT / "solver.npz", **rec)
+
+    # ---- conv ----------------------------------------------------------------
+    rng = np.random.default_rng(3)
+    stack = f32(rng.uniform(size=(4, 8, 9)))
+    rec = {"stack": stack}
+    for k, (l1, l2) in enumerate(((3, 3), (2, 4), (5, 5), (7, 7))):
+        filt = f32(rng.standard_normal((3, l1, l2)))
+        rec[f"filt{k}"] = filt
+        for center in (False, True):
+            layer = FilterLayer(filters1=filt, filters2=filt, geom=dd.PatchGeometry(l1, l2), center=center)
+            rec[f"out{k}_{int(center)}"] = apply_filters(stack, layer, view=1)
+    np.savez_compressed(OUT / "conv.npz", **rec)
+
+    # ---- encoder -------------------------------------------------------------
+    rng = np.random.default_rng(2)
+    maps = f32(rng.standard_normal((8, 8, 10)))
+    rec = {"maps": maps}
+    for k, (bh, bw, ov, pol, nb) in enumerate(((4, 4, 0.0, "zero", 4), (4, 4, 0.0, "floor", 4),
+                                                (4, 4, 0.5, "zero", 2), (3, 5, 0.0, "zero", 8),
+                                                (2, 2, 0.25, "floor", 1))):
+        cfg = dd.EncoderConfig(block_h=bh, block_w=bw, overlap=ov, zero_bin_policy=pol)
+        rec[f"cfg{k}"] = np.array([bh, bw, ov, 1.0 if pol == "floor" else 0.0, nb])
+        rec[f"feat{k}"] = dd.encode_view(maps, nb, cfg)
+    np.savez_compressed(OUT / "encoder.npz", **rec)
+
+    # ---- pipeline: fit + transform on small datasets ---------------------------
+    def run_pipeline(name, v1, v2, labels, classes, layer_specs, batch, bh, bw):
+        samples = [dd.ViewPairSample(view1=v1[i], view2=v2[i], label=int(labels[i])) for i in range(len(labels))]
+        ds = dd.ViewPairDataset(samples=samples, class_count=classes)
+        net = dd.NetworkConfig(
+            layers=tuple(dd.LayerConfig(filters=L, geom=dd.PatchGeometry(l1, l2)) for L, l1, l2 in layer_specs),
+            batch=dd.BatchSpec(batch))
+        cfg = types.SimpleNamespace(net=net, encoder=dd.EncoderConfig(block_h=bh, block_w=bw))
+        with dd.Executor(dd.ExecSettings(threads=1)) as ex:
+            bank = dd.train_network(ds, net, ex)
+            feats = compute_features(ds, bank, cfg, ex)
+            acc1 = dd.cascade.accumulate_layer_moments(layer_input(ds), net.layers[0].geom, True, classes,
+                                                       net.batch, ex)
+            fin1 = dd.finalize(acc1, 1e-4)
+        rec = {"v1": v1, "v2": v2, "labels": labels, "classes": classes, "batch": batch,
+               "layers": np.array(layer_specs), "block": np.array([bh, bw]), "features": feats,
+               "acc1_c11": acc1.c11, "acc1_c22": acc1.c22, "acc1_s1": acc1.class_sum1,
+               "acc1_s2": acc1.class_sum2, "acc1_g1": acc1.global_sum1, "acc1_g2": acc1.global_sum2,
+               "acc1_n": acc1.patch_count, "fin1_ct": fin1.ctilde}
+        for i, layer in enumerate(bank.layers):
+            rec[f"f1_{i}"] = layer.filters1
+            rec[f"f2_{i}"] = layer.filters2
+        np.savez_compressed(OUT / f"{name}.npz", **rec)
+
+    rng = np.random.default_rng(9)
+    v1 = f32(rng.uniform(size=(24, 12, 10)))
+    v2 = f32(rng.uniform(size=(24, 12, 10)))
+    run_pipeline("pipeline_small", v1, v2, np.arange(24) % 3, 3, [(4, 3, 3), (2, 3, 3)], 8, 4, 4)
+
+    imgs, labels = rect_blobs(40, 28, 23, 4, seed=0)
+    v1 = f32(imgs)
+    v2 = f32(np.stack([dd.lbp_map(im) for im in v1]))
+    run_pipeline("pipeline_orl_mini", v1, v2, labels, 4, [(4, 5, 5), (4, 5, 5)], 16, 7, 7)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()
