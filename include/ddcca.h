@@ -1,0 +1,195 @@
+/*
+ * ddcca.h — C ABI of the B200-native DDCCANet fit/transform path.
+ *
+ * The reference (ddccanet 0.1.0, pure Python/numpy) has no native FFI; its
+ * boundary is the Python API of cascade/moments/solver/encoder/pipeline.
+ * Every entry point below replaces one reference function (file:line under
+ * /root/reference/pkg/src/ddccanet/) and is bound from Python with ctypes
+ * (paper_2209_13027_b200/_native.py; see INTEGRATION.md for the stub a
+ * reference maintainer would add).
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (sm_100a, same CUDA context as
+ *     the caller), except where a name ends in `_host`.
+ *   - `stream` is a cudaStream_t passed as void*; all work is stream-ordered
+ *     and asynchronous unless stated. The library keeps no global mutable
+ *     state: scratch memory is passed in (`ws`, `ws_bytes`), so calls are
+ *     re-entrant across streams and threads.
+ *   - Return codes: DDCCA_OK, DDCCA_ESHAPE (reference ShapeError),
+ *     DDCCA_ECONFIG (ConfigError), DDCCA_ENUMERICAL (NumericalError),
+ *     DDCCA_ECUDA (launch/runtime failure). ddcca_last_error() returns a
+ *     thread-local message for the last failing call on this thread.
+ *   - Moment payload (one "accumulator", float64, length ddcca_payload_len):
+ *       [ c11 (d*d) | c22 (d*d) | s1 (d*C, row-major d x C) | s2 (d*C) |
+ *         g1 (d) | g2 (d) | patch_count (1) | per_class_count (C) ]
+ *     i.e. the fields of MomentAccumulator (moments.py:26-48). Counts are
+ *     stored as float64 (exact below 2^53 patches).
+ */
+#ifndef DDCCA_H
+#define DDCCA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DDCCA_API __attribute__((visibility("default")))
+#else
+#define DDCCA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DDCCA_OK = 0,
+  DDCCA_ESHAPE = 1,
+  DDCCA_ECONFIG = 2,
+  DDCCA_ENUMERICAL = 3,
+  DDCCA_ECUDA = 4
+};
+
+/* Library ABI version (bumped on any signature change). */
+DDCCA_API int ddcca_version(void);
+
+/* Thread-local message of the last failing call on this thread. */
+DDCCA_API const char* ddcca_last_error(void);
+
+/* Length in float64 of one moment payload for (dim, class_count). */
+DDCCA_API int64_t ddcca_payload_len(int dim, int class_count);
+
+/* Geometry shared by the patch-based kernels; restates PatchGeometry
+ * (patches.py:22-65): zero_same pads top=(l1-1)//2, left=(l2-1)//2, output
+ * grid ceil(p/stride) x ceil(q/stride); padding "none" has no pads. */
+typedef struct {
+  int p, q;            /* map height, width */
+  int l1, l2;          /* window height, width */
+  int stride;          /* >= 1 */
+  int zero_same;       /* 1 = "zero_same", 0 = "none" */
+} ddcca_geom;
+
+/* ---------------------------------------------------------------------
+ * K1+K2+K3 — per-batch partial moments
+ * Replaces: cascade._batch_accumulator_job / accumulate_layer_moments
+ *           (cascade.py:155-189) including extract_patch_stack
+ *           (patches.py:97-125) and accumulate_batch (moments.py:86-110).
+ * maps1/maps2: (n_maps, p, q) float32, view 1 / view 2, maps of one sample
+ *   contiguous, samples in manifest order.
+ * map_label: (n_maps,) int32 class of each map, in [0, class_count).
+ * batch_offsets_host: HOST array (n_batches+1) of map offsets; batch b is
+ *   maps [off[b], off[b+1]) (the BatchSpec partition, patches.py:148-157).
+ * partials: (n_batches, payload_len) float64 output, one accumulator per
+ *   batch — the reference's per-batch MomentAccumulator.
+ * center: subtract each patch's mean (extract_patch_stack center=True).
+ * Stride-1 geometries use the exact windowed-autocorrelation form (float64
+ * products of float32 inputs are exact); other strides use explicit
+ * float64 patch columns. Deterministic: fixed reduction order.
+ * ------------------------------------------------------------------- */
+DDCCA_API size_t ddcca_moments_workspace(const ddcca_geom* g, int n_batches, int64_t max_maps_per_batch,
+                               int class_count);
+DDCCA_API int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t* map_label,
+                          const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* g,
+                          int center, int class_count, double* partials, void* ws, size_t ws_bytes,
+                          void* stream);
+
+/* ---------------------------------------------------------------------
+ * K9 — fixed left-to-right pairwise tree over n_parts payloads
+ * Replaces: pairwise_merge (moments.py:132-144); merge (moments.py:113-129)
+ * is the n_parts == 2 case. parts is overwritten (in-place tree); the
+ * result is copied to out.
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_moments_tree(double* parts, int n_parts, int64_t payload_len, double* out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Explicit patch columns (API-level accumulate_batch, moments.py:86-110)
+ * x, y: (dim, cols) float64 row-major; labels: (cols,) int64.
+ * Adds into payload (in place).
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_accumulate_columns(const double* x, const double* y, const int64_t* labels, int64_t cols,
+                             int dim, int class_count, double* payload, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K4+K5 — finalize + DCCA solve on device (single CTA, float64 Jacobi)
+ * Replaces: finalize (moments.py:168-193), solve_dcca (solver.py:216-257),
+ *           sym_eig / inv_sqrt (solver.py:90-170), reshape_filters
+ *           (solver.py:260-272).
+ * payload: one merged accumulator. Outputs (all device, float64 unless
+ * noted): fin (5*d*d: c11, c22, cw, cb, ctilde — DiscriminantMoments),
+ * w1, w2 (d x count, row-major), rho (count), conv_pack (float32, see
+ * ddcca_conv) for both views, status (int32: DDCCA_* code; 0 = ok).
+ * payload == NULL: skip finalize and solve from the moments already in
+ * `fin` (API-level solve_dcca(DiscriminantMoments, count)).
+ * Needs ddcca_solve_workspace(d) bytes of scratch.
+ * ------------------------------------------------------------------- */
+DDCCA_API size_t ddcca_solve_workspace(int dim);
+DDCCA_API int ddcca_solve(const double* payload, int dim, int class_count, double epsilon, int count,
+                double* fin, double* w1, double* w2, double* rho, float* conv_pack1, float* conv_pack2,
+                int32_t* status, void* ws, size_t ws_bytes, void* stream);
+
+/* finalize only (moments.py:168-193): fin = [c11 | c22 | cw | cb | ctilde]. */
+DDCCA_API int ddcca_finalize(const double* payload, int dim, int class_count, double epsilon, double* fin,
+                             int32_t* status, void* stream);
+
+/* Sign binarization + LSB-first hash of consecutive groups of n_bits maps
+ * (binarize + hash_combine, encoder.py:50-68): maps (n_groups*n_bits, plane)
+ * float32 -> codes (n_groups, plane) uint8 (n_bits <= 8) or uint16. */
+DDCCA_API int ddcca_sign_hash(const float* maps, int64_t n_groups, int n_bits, int64_t plane, void* codes,
+                              void* stream);
+
+/* Standalone symmetric eigensolver (sym_eig, solver.py:90-158) and
+ * inverse square root (inv_sqrt, solver.py:161-170) on one n x n matrix.
+ * mode 0: w (n), v (n x n); mode 1: r = inv_sqrt(s) into v, w = eigvals. */
+DDCCA_API int ddcca_sym_eig(const double* s, int n, int mode, double* w, double* v, int32_t* status, void* ws,
+                  size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K6 — multi-filter convolution with per-window centering
+ * Replaces: apply_filters (cascade.py:108-126) / conv2d (cascade.py:93-100).
+ * in: (n_maps, p, q) float32. out: (n_maps, count, oh, ow) float32,
+ * filter-minor (children of one input map contiguous, cascade.py:123-125).
+ * conv_pack: float32 [d][count] weights (tap-major) as written by
+ * ddcca_solve or ddcca_pack_filters.
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_pack_filters(const double* filters, int count, int dim, float* conv_pack, void* stream);
+DDCCA_API int ddcca_conv(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack, int count,
+               int center, float* out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K6-final + K7 — last-layer conv fused with sign binarization and the
+ * LSB-first 2^count hash (encoder.py:50-68, cascade.py:108-126).
+ * codes: (n_maps, oh, ow) uint8 when count <= 8, else uint16.
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_conv_hash(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack, int count,
+                    int center, void* codes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K8 — block histograms of code maps (iq_block_features counts,
+ * encoder.py:71-99; block_starts encoder.py:38-44).
+ * codes: (n_groups, oh, ow), code_bytes 1 or 2. Output counts for group k
+ * at counts + (k / groups_per_row) * row_stride + (k % groups_per_row) *
+ * group_stride (elements), laid out [block][bin]. count_kind: 0 = uint8
+ * (bpc <= 255), 1 = saturating uint8 (256 <= bpc <= 510: 255 means "255 +
+ * remainder of the block"), 2 = uint16.
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_block_hist(const void* codes, int code_bytes, int64_t n_groups, int oh, int ow, int n_bits,
+                     int block_h, int block_w, int step_h, int step_w, void* counts, int count_kind,
+                     int64_t groups_per_row, int64_t row_stride, int64_t group_stride, void* stream);
+
+/* Counts -> float64 IQ features through a host-built LUT of bpc+1 values
+ * (lut[0] = zero-bin value, lut[k] = -log(k/bpc)), encoder.py:87-97.
+ * n_blocks histograms of 2^n_bits bins each, contiguous. */
+DDCCA_API int ddcca_iq_expand(const void* counts, int count_kind, int64_t n_blocks, int n_bits, int bpc,
+                    const double* lut, double* out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * K1 standalone — explicit patch matrix (extract_patch_stack,
+ * patches.py:97-125): maps (n_maps, p, q) float64 -> out (dim, n_maps*oh*ow)
+ * float64 row-major.
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_im2col(const double* maps, int64_t n_maps, const ddcca_geom* g, int center, double* out,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDCCA_H */

@@ -1,0 +1,272 @@
+"""Layer-wise training and application of the two-view filter cascade.
+
+API mirror of cascade.py:26-259 of the reference, backed by the device
+engine (engine.py). ``train_network`` is the fit entry point and
+``pipeline.compute_features`` the transform entry point; everything between
+the host arrays and the returned FilterBank / features runs as sm_100a
+kernels. Maps are stored as float32 on the device (the reference keeps
+float64 on the host); statistics and the solve are float64.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import engine as E
+from .errors import ConfigError, ShapeError
+from .patches import BatchSpec, PatchGeometry, batch_partition
+from .solver import FilterBank, FilterLayer
+
+CHUNK_COLS = 1 << 17  # reference chunking constant (cascade.py:26); the device path needs no chunks
+
+
+@dataclass(frozen=True)
+class LayerConfig:
+    """Filter count, window geometry, centering (cascade.py:29-41)."""
+
+    filters: int
+    geom: PatchGeometry
+    center: bool = True
+
+    def __post_init__(self):
+        if self.filters < 1:
+            raise ConfigError(f"filter count {self.filters} must be >= 1")
+        if self.filters > self.geom.dim:
+            raise ConfigError(f"filter count {self.filters} exceeds patch dimension {self.geom.dim}")
+
+
+@dataclass(frozen=True)
+class NetworkConfig:
+    """Layers, sample batching, ridge (cascade.py:44-52)."""
+
+    layers: tuple
+    batch: BatchSpec = BatchSpec()
+    epsilon: float = 1e-4
+
+    def __post_init__(self):
+        if not self.layers:
+            raise ConfigError("network needs at least one layer")
+
+
+@dataclass
+class LayerOutput:
+    """Maps of both views for a set of samples plus lineage (cascade.py:55-80)."""
+
+    maps1: np.ndarray
+    maps2: np.ndarray
+    labels: np.ndarray
+    lineage: tuple
+
+    def __post_init__(self):
+        if self.maps1.shape != self.maps2.shape:
+            raise ShapeError(f"view map stacks differ: {self.maps1.shape} vs {self.maps2.shape}")
+        if len(self.lineage) != self.maps1.shape[1]:
+            raise ShapeError("one lineage entry per map required")
+
+    @property
+    def n_samples(self) -> int:
+        return self.maps1.shape[0]
+
+    @property
+    def n_maps(self) -> int:
+        return self.maps1.shape[1]
+
+    @property
+    def map_shape(self) -> tuple[int, int]:
+        return self.maps1.shape[2], self.maps1.shape[3]
+
+
+def _child_lineage(lineage, count: int):
+    return tuple(parent + (g,) for parent in lineage for g in range(count))
+
+
+def layer_input(ds) -> LayerOutput:
+    """Dataset as first-layer input: one map per view (cascade.py:83-90)."""
+    v1, v2, lab = ds.stacks_view()
+    return LayerOutput(maps1=np.asarray(v1)[:, None], maps2=np.asarray(v2)[:, None], labels=np.asarray(lab),
+                       lineage=((),))
+
+
+def _executor(executor):
+    from .execution import Executor
+
+    return executor if executor is not None and hasattr(executor, "stream") else Executor()
+
+
+def _to_dev32(ex, a):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
+    return t.to(ex.device, non_blocking=True) if t.is_pinned() else t.to(ex.device)
+
+
+def _labels_dev(ex, labels):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(labels, dtype=np.int32))).to(ex.device)
+
+
+def device_layers(bank: FilterBank, ex) -> list:
+    """DeviceLayers for a bank (cached on the bank per device)."""
+    cache = getattr(bank, "_device_cache", None)
+    if cache is not None and cache[0] == str(ex.device):
+        return cache[1]
+    layers = [E.layer_from_filters(ex, l.filters1, l.filters2, l.geom, l.center) for l in bank.layers]
+    object.__setattr__(bank, "_device_cache", (str(ex.device), layers))
+    return layers
+
+
+def _bank_from_device(layers: list) -> FilterBank:
+    out = []
+    for lay in layers:
+        w1 = lay.w1.cpu().numpy()
+        w2 = lay.w2.cpu().numpy()
+        L, g = lay.count, lay.geom
+        out.append(FilterLayer(filters1=np.ascontiguousarray(w1.T).reshape(L, g.l1, g.l2).copy(),
+                               filters2=np.ascontiguousarray(w2.T).reshape(L, g.l1, g.l2).copy(),
+                               geom=g, center=lay.center))
+    return FilterBank(layers=tuple(out))
+
+
+def conv2d(plane, kernel, padding: str = "zero_same", center: bool = False, executor=None) -> np.ndarray:
+    """Cross-correlate one map with one kernel (cascade.py:93-100)."""
+    kernel = np.asarray(kernel, dtype=np.float64)
+    if kernel.ndim != 2:
+        raise ShapeError(f"kernel must be 2-D, got shape {kernel.shape}")
+    geom = PatchGeometry(kernel.shape[0], kernel.shape[1], 1, padding)
+    layer = FilterLayer(kernel[None], kernel[None], geom, center)
+    return apply_filters(np.asarray(plane, dtype=np.float64)[None], layer, 1, executor)[0, 0]
+
+
+def apply_filters(stack, layer: FilterLayer, view: int, executor=None) -> np.ndarray:
+    """(N, p, q) -> (N, L, p', q') filter-minor (cascade.py:108-126), float32 device conv."""
+    import torch
+
+    stack = np.asarray(stack)
+    if stack.ndim != 3:
+        raise ShapeError(f"expected (N, p, q) maps, got shape {stack.shape}")
+    ex = _executor(executor)
+    with torch.cuda.stream(ex.stream):
+        dl = E.layer_from_filters(ex, layer.filters1, layer.filters2, layer.geom, layer.center)
+        out = E.conv(ex, _to_dev32(ex, stack), dl, view)
+        return out.cpu().numpy().astype(np.float64)
+
+
+def apply_layer(inputs: LayerOutput, layer: FilterLayer, executor, batch: BatchSpec) -> LayerOutput:
+    """Run one trained layer over all samples (cascade.py:133-152)."""
+    n, m = inputs.n_samples, inputs.n_maps
+    p, q = inputs.map_shape
+    o1 = apply_filters(inputs.maps1.reshape(-1, p, q), layer, 1, executor)
+    o2 = apply_filters(inputs.maps2.reshape(-1, p, q), layer, 2, executor)
+    oh, ow = o1.shape[2:]
+    return LayerOutput(maps1=o1.reshape(n, m * layer.count, oh, ow), maps2=o2.reshape(n, m * layer.count, oh, ow),
+                       labels=inputs.labels, lineage=_child_lineage(inputs.lineage, layer.count))
+
+
+def accumulate_layer_moments(inputs: LayerOutput, geom: PatchGeometry, center: bool, class_count: int,
+                             batch: BatchSpec, executor):
+    """Per-batch moments of a layer's input maps merged by the fixed tree (cascade.py:155-189)."""
+    import torch
+
+    from .moments import MomentAccumulator
+
+    ex = _executor(executor)
+    n, m = inputs.n_samples, inputs.n_maps
+    p, q = inputs.map_shape
+    lab = np.asarray(inputs.labels)
+    if lab.size and (lab.min() < 0 or lab.max() >= class_count):
+        raise ShapeError(f"label outside [0, {class_count})")
+    ranges = batch_partition(n, batch)
+    with torch.cuda.stream(ex.stream):
+        m1 = _to_dev32(ex, inputs.maps1.reshape(-1, p, q))
+        m2 = _to_dev32(ex, inputs.maps2.reshape(-1, p, q))
+        mlab = _labels_dev(ex, np.repeat(lab, m))
+        offs = np.array([0] + [r.stop * m for r in ranges], dtype=np.int64)
+        parts = E.moments_partials(ex, m1, m2, mlab, offs, geom, center, class_count)
+        merged = E.tree_merge(ex, parts).cpu().numpy()
+    return MomentAccumulator.from_payload(merged, geom.dim, class_count)
+
+
+def train_layer(inputs: LayerOutput, cfg: LayerConfig, class_count: int, batch: BatchSpec, executor,
+                epsilon: float = 1e-4) -> FilterLayer:
+    """One layer's filters from its input maps (cascade.py:192-204)."""
+    import torch
+
+    ex = _executor(executor)
+    n, m = inputs.n_samples, inputs.n_maps
+    p, q = inputs.map_shape
+    ranges = batch_partition(n, batch)
+    with torch.cuda.stream(ex.stream):
+        m1 = _to_dev32(ex, inputs.maps1.reshape(-1, p, q))
+        m2 = _to_dev32(ex, inputs.maps2.reshape(-1, p, q))
+        mlab = _labels_dev(ex, np.repeat(np.asarray(inputs.labels), m))
+        offs = np.array([0] + [r.stop * m for r in ranges], dtype=np.int64)
+        parts = E.moments_partials(ex, m1, m2, mlab, offs, cfg.geom, cfg.center, class_count)
+        merged = E.tree_merge(ex, parts)
+        lay = E.solve_layer(ex, merged, cfg.geom, cfg.filters, cfg.center, class_count, epsilon)
+        return _bank_from_device([lay]).layers[0]
+
+
+def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBank:
+    """Fit: train all layers bottom-up on the device (cascade.py:207-223).
+
+    Intermediate layers are not materialized for the whole training set:
+    each layer's input maps are recomputed per super-batch from the images
+    (the conv is cheaper than writing and re-reading them), so memory stays
+    bounded for any corpus size. With a torch.distributed process group the
+    samples are sharded by whole batches over the ranks and the per-layer
+    partial moments are reduced with NCCL before the solve.
+    """
+    import torch
+
+    ex = _executor(executor)
+    v1, v2, lab = ds.stacks_view()
+    lab = np.asarray(lab)
+    if lab.size and (lab.min() < 0 or lab.max() >= ds.class_count):
+        raise ShapeError(f"label outside [0, {ds.class_count})")
+    n = len(lab)
+    bs = cfg.batch.batch_size
+    gb = batch_partition(n, cfg.batch)
+    mine = ex.shard(len(gb))
+    s0 = gb[mine.start].start if len(mine) else 0
+    s1 = gb[mine.stop - 1].stop if len(mine) else 0
+    eng = E.Engine(ex)
+    with torch.cuda.stream(ex.stream):
+        i1 = _to_dev32(ex, np.asarray(v1)[s0:s1])
+        i2 = _to_dev32(ex, np.asarray(v2)[s0:s1])
+        ld = _labels_dev(ex, lab[s0:s1])
+        res = eng.fit(i1, i2, ld, ds.class_count, list(cfg.layers), bs, cfg.epsilon, n_global=n, first_sample=s0,
+                      stage_hook=stage_hook)
+    bank = _bank_from_device(res.layers)
+    object.__setattr__(bank, "_device_cache", (str(ex.device), res.layers))
+    return bank
+
+
+def forward_stacks(view1, view2, bank: FilterBank, executor=None):
+    """(B, p, q) views through every layer -> (B, n_maps, p', q') each (cascade.py:226-235)."""
+    import torch
+
+    ex = _executor(executor)
+    v1 = np.asarray(view1)
+    b = v1.shape[0]
+    with torch.cuda.stream(ex.stream):
+        layers = device_layers(bank, ex)
+        m1 = E.forward_maps(ex, _to_dev32(ex, v1), layers, 1)
+        m2 = E.forward_maps(ex, _to_dev32(ex, view2), layers, 2)
+        r1 = m1.reshape(b, -1, m1.shape[1], m1.shape[2]).cpu().numpy().astype(np.float64)
+        r2 = m2.reshape(b, -1, m2.shape[1], m2.shape[2]).cpu().numpy().astype(np.float64)
+    return r1, r2
+
+
+def forward(ds, bank: FilterBank, executor, batch: BatchSpec) -> LayerOutput:
+    """Final-layer maps for the whole dataset (cascade.py:238-259)."""
+    v1, v2, lab = ds.stacks_view()
+    parts = [forward_stacks(np.asarray(v1)[r.start:r.stop], np.asarray(v2)[r.start:r.stop], bank, executor)
+             for r in batch_partition(len(ds), batch)]
+    lineage = ((),)
+    for layer in bank.layers:
+        lineage = _child_lineage(lineage, layer.count)
+    return LayerOutput(maps1=np.concatenate([a for a, _ in parts]), maps2=np.concatenate([b for _, b in parts]),
+                       labels=np.asarray(lab), lineage=lineage)

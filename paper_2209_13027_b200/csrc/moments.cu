@@ -1,0 +1,902 @@
+// K1+K2+K3: per-batch DDCCA moments from image maps, without materializing
+// patches.
+//
+// Reference semantics (cascade.py:155-189, patches.py:97-125,
+// moments.py:86-110): for every batch of samples, every stride-1 window of
+// every map yields a patch x (d = l1*l2, zero padding counted), centered by
+// its own mean when `center`; C11 += x x^T (view 1), C22 += y y^T (view 2),
+// class / global column sums, counts.
+//
+// B200 formulation. For stride 1 the raw Gram is a windowed
+// autocorrelation of the padded map P (Hp x Wp):
+//   Craw[(a,b),(a+dy,b+dx)] = sum_{y in [a,a+oh), x in [b,b+ow)} P[y,x] P[y+dy,x+dx]
+// and centering is the exact projection C = H Craw H, H = I - 11^T/d
+// (H kills constants, patch by patch). Each first pixel (y,x) contributes to
+// a rectangle of (a,b) that depends only on its row zone / column zone (the
+// runs of rows/cols with equal a-range / b-range). So per batch we only need,
+// for every lag (dy,dx) and every (row zone, col zone), the sum of
+// P[y,x] P[y+dy,x+dx] over that zone: l1*(2*l2-1) lags x ~(2l1-1)(2l2-1)
+// zones, instead of d^2/2 products per patch. float32 inputs make every
+// product exact in float64; sums are float64, so the result matches the
+// reference's float64 Gram to ~1e-15 relative before centering.
+//
+// Kernels:
+//   lag_zone_kernel   one block per (task, split, batch, view): a task is a
+//                     row range of one row zone x a 32-column tile; the block
+//                     loops over its maps, keeps per-thread float64
+//                     accumulators (l1 x KDX lags) and writes one record per
+//                     (task, column zone present in the tile).
+//   zone_reduce       records -> Z[batch][view][rz][cz][lag] (fixed order).
+//   assemble          Z -> Craw -> H Craw H -> payload c11/c22.
+//   rect_sums         per-map window sums (class-sum path), centered.
+//   batch_epilogue    per-batch class sums / global sums / counts.
+//   direct_*          explicit-patch float64 path for stride != 1.
+#include <vector>
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ddcca {
+
+constexpr int KDX = 3;       // dx lags per thread
+constexpr int TILE_X = 32;   // first-pixel columns per block (one per lane)
+constexpr int SLAB_Y = 32;   // max first-pixel rows per interior task
+constexpr int MAPS_PER_SPLIT = 128;
+constexpr int MAX_LAG_L = 12;  // lag path for windows up to 12 x 12
+
+struct Zones {
+  // zone index of each padded row / column and each zone's a-/b-range
+  std::vector<int> rz_of_y, cz_of_x;
+  std::vector<int> rz_lo, rz_hi, cz_lo, cz_hi;
+  int big_cz = -1;  // column zone with >= 2 columns (the interior), or -1
+};
+
+static void make_zones(int n, int out, int l, std::vector<int>& zone_of, std::vector<int>& lo,
+                       std::vector<int>& hi) {
+  zone_of.assign(n, 0);
+  lo.clear();
+  hi.clear();
+  int prev_lo = -1, prev_hi = -1;
+  for (int y = 0; y < n; ++y) {
+    int a_lo = std::max(0, y - out + 1), a_hi = std::min(y, l - 1);
+    if (a_lo != prev_lo || a_hi != prev_hi) {
+      lo.push_back(a_lo);
+      hi.push_back(a_hi);
+      prev_lo = a_lo;
+      prev_hi = a_hi;
+    }
+    zone_of[y] = (int)lo.size() - 1;
+  }
+}
+
+struct Task {
+  int y0, y1, x0, rz;
+  int rec0;     // first record index of this task within a (batch, split)
+  int nrec;     // records written: [big zone if present] + singleton columns
+};
+
+// A record: sum over one task's rows and over the lanes of one column zone.
+struct RecInfo {
+  int rz, cz;
+};
+
+struct Plan {
+  Geo g;
+  Zones z;
+  int nrz, ncz, G, NDX, NDF;
+  std::vector<Task> tasks;
+  std::vector<RecInfo> recs;
+  std::vector<int> lane_slot;  // per task * 32 + lane -> record offset within task, or -1 (big zone)
+  int nrec;
+};
+
+static void make_plan(const Geo& g, Plan* P) {
+  P->g = g;
+  make_zones(g.Hp, g.oh, g.l1, P->z.rz_of_y, P->z.rz_lo, P->z.rz_hi);
+  make_zones(g.Wp, g.ow, g.l2, P->z.cz_of_x, P->z.cz_lo, P->z.cz_hi);
+  P->nrz = (int)P->z.rz_lo.size();
+  P->ncz = (int)P->z.cz_lo.size();
+  // column zone with the most columns becomes the warp-reduced "big" zone
+  std::vector<int> ccount(P->ncz, 0);
+  for (int x = 0; x < g.Wp; ++x) ccount[P->z.cz_of_x[x]]++;
+  int best = -1, bestn = 1;
+  for (int c = 0; c < P->ncz; ++c)
+    if (ccount[c] > bestn) { bestn = ccount[c]; best = c; }
+  P->z.big_cz = best;
+  P->G = (2 * g.l2 - 1 + KDX - 1) / KDX;
+  P->NDX = P->G * KDX;
+  P->NDF = g.l1 * P->NDX;
+  P->tasks.clear();
+  P->recs.clear();
+  P->lane_slot.clear();
+  int nrec = 0;
+  int y = 0;
+  while (y < g.Hp) {
+    int rz = P->z.rz_of_y[y];
+    int y_end = y;
+    while (y_end < g.Hp && P->z.rz_of_y[y_end] == rz) ++y_end;
+    for (int ys = y; ys < y_end; ys += SLAB_Y) {
+      int ye = std::min(y_end, ys + SLAB_Y);
+      for (int x0 = 0; x0 < g.Wp; x0 += TILE_X) {
+        Task t;
+        t.y0 = ys; t.y1 = ye; t.x0 = x0; t.rz = rz; t.rec0 = nrec; t.nrec = 0;
+        bool has_big = false;
+        for (int l = 0; l < TILE_X; ++l) {
+          int x = x0 + l;
+          if (x < g.Wp && P->z.cz_of_x[x] == P->z.big_cz) has_big = true;
+        }
+        if (has_big) {
+          P->recs.push_back({rz, P->z.big_cz});
+          t.nrec++;
+        }
+        for (int l = 0; l < TILE_X; ++l) {
+          int x = x0 + l;
+          if (x < g.Wp && P->z.cz_of_x[x] != P->z.big_cz) {
+            P->lane_slot.push_back(t.nrec);
+            P->recs.push_back({rz, P->z.cz_of_x[x]});
+            t.nrec++;
+          } else {
+            P->lane_slot.push_back(-1);
+          }
+        }
+        nrec += t.nrec;
+        P->tasks.push_back(t);
+      }
+    }
+    y = y_end;
+  }
+  P->nrec = nrec;
+}
+
+// ----------------------------------------------------------------------------
+// lag_zone_kernel
+// ----------------------------------------------------------------------------
+struct TaskDev {
+  int y0, y1, x0, rec0;
+};
+
+struct LagArgs {
+  const float* maps[2];
+  const TaskDev* tasks;
+  const int* lane_slot;     // [task][32]
+  const int64_t* batch_off; // device copy of batch map offsets
+  double* rec;              // [batch][view][split][nrec][NDF]
+  int p, q, top, left, Wp, l2, G, NDX, NDF, nrec, nsplit, nbatch;
+};
+
+template <int L1>
+__global__ void __launch_bounds__(256) lag_zone_kernel(LagArgs A) {
+  extern __shared__ double tile[];
+  const int task = blockIdx.x;
+  const int split = blockIdx.y;
+  const int bv = blockIdx.z;  // batch * 2 + view
+  const int batch = bv >> 1, view = bv & 1;
+  const TaskDev T = A.tasks[task];
+  const int lane = threadIdx.x & 31;
+  const int grp = threadIdx.x >> 5;
+  const int nrows = T.y1 - T.y0;
+  const int tr = nrows + L1 - 1;                  // staged rows
+  const int tc = TILE_X + A.NDX - 1;              // staged cols: [x0-(l2-1), x0-(l2-1)+tc)
+  const int xs = T.x0 - (A.l2 - 1);
+  const int64_t m_begin = A.batch_off[batch];
+  const int64_t m_end = A.batch_off[batch + 1];
+  const int64_t per = (m_end - m_begin + A.nsplit - 1) / A.nsplit;
+  const int64_t ma = m_begin + (int64_t)split * per;
+  const int64_t mb = min(m_end, ma + per);
+  const float* src = view == 0 ? A.maps[0] : A.maps[1];
+  const int plane = A.p * A.q;
+
+  double acc[L1][KDX];
+#pragma unroll
+  for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+    for (int k = 0; k < KDX; ++k) acc[dy][k] = 0.0;
+
+  const int cown = lane + (A.l2 - 1);  // own column inside the tile
+  const int cpart = lane + grp * KDX;  // partner column of k = 0
+
+  for (int64_t m = ma; m < mb; ++m) {
+    const float* img = src + m * (int64_t)plane;
+    __syncthreads();
+    for (int e = threadIdx.x; e < tr * tc; e += blockDim.x) {
+      int r = e / tc, c = e - r * tc;
+      int i = T.y0 + r - A.top, j = xs + c - A.left;
+      float v = 0.f;
+      if (i >= 0 && i < A.p && j >= 0 && j < A.q) v = __ldg(img + (int64_t)i * A.q + j);
+      tile[e] = (double)v;
+    }
+    __syncthreads();
+    if (grp >= A.G) continue;
+    double ring[L1][KDX];
+#pragma unroll
+    for (int s = 0; s < L1 - 1; ++s)
+#pragma unroll
+      for (int k = 0; k < KDX; ++k) ring[s][k] = tile[s * tc + cpart + k];
+    for (int r0 = 0; r0 < nrows; r0 += L1) {
+#pragma unroll
+      for (int u = 0; u < L1; ++u) {
+        const int r = r0 + u;
+        if (r < nrows) {
+          const int snew = (u + L1 - 1) % L1;
+#pragma unroll
+          for (int k = 0; k < KDX; ++k) ring[snew][k] = tile[(r + L1 - 1) * tc + cpart + k];
+          const double own = tile[r * tc + cown];
+#pragma unroll
+          for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+            for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, ring[(u + dy) % L1][k], acc[dy][k]);
+        }
+      }
+    }
+  }
+  if (grp >= A.G) return;
+  // lanes outside the map's padded width hold zeros already (tile zero-filled)
+  const int slot = A.lane_slot[task * TILE_X + lane];
+  const int x = T.x0 + lane;
+  const bool in_big = (slot < 0) && (x < A.Wp);
+  double* out = A.rec + (((int64_t)batch * 2 + view) * A.nsplit + split) * (int64_t)A.nrec * A.NDF;
+  // big-zone record index is rec0 (the task's first record) when present
+#pragma unroll
+  for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+    for (int k = 0; k < KDX; ++k) {
+      const int lag = dy * A.NDX + grp * KDX + k;
+      double v = in_big ? acc[dy][k] : 0.0;
+      v = warp_sum(v);
+      const int any_big = __any_sync(0xffffffffu, in_big);
+      if (lane == 0 && any_big) out[(int64_t)T.rec0 * A.NDF + lag] = v;
+      if (slot >= 0) out[(int64_t)(T.rec0 + slot) * A.NDF + lag] = acc[dy][k];
+    }
+}
+
+// ----------------------------------------------------------------------------
+// zone_reduce: Z[batch][view][rz][cz][lag] = sum over splits, records (fixed order)
+// ----------------------------------------------------------------------------
+__global__ void zone_reduce_kernel(const double* __restrict__ rec, const int* __restrict__ zrec_off,
+                                   const int* __restrict__ zrec_list, double* __restrict__ Z, int nzone,
+                                   int NDF, int nrec, int nsplit) {
+  const int bv = blockIdx.y;
+  const int64_t total = (int64_t)nzone * NDF;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int zone = (int)(e / NDF), lag = (int)(e % NDF);
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const double* base = rec + ((int64_t)bv * nsplit + sp) * (int64_t)nrec * NDF;
+      for (int t = zrec_off[zone]; t < zrec_off[zone + 1]; ++t) s += base[(int64_t)zrec_list[t] * NDF + lag];
+    }
+    Z[(int64_t)bv * total + e] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// assemble: Craw (canonical half, mirrored) -> centered -> payload c11 / c22
+// ----------------------------------------------------------------------------
+struct AsmArgs {
+  const double* Z;
+  const int* rz_lo; const int* rz_hi; const int* cz_lo; const int* cz_hi;
+  double* payload;  // [batch][payload_len]
+  int64_t plen;
+  int nrz, ncz, NDX, NDF, l1, l2, d, center;
+};
+
+__global__ void assemble_kernel(AsmArgs A) {
+  extern __shared__ double sm[];
+  double* C = sm;                    // d*d raw then centered
+  double* rs = sm + A.d * A.d;       // row sums (d)
+  const int bv = blockIdx.x;
+  const int batch = bv >> 1, view = bv & 1;
+  const double* Z = A.Z + (int64_t)bv * A.nrz * A.ncz * A.NDF;
+  const int d = A.d;
+  // canonical entries: i = (a,b), j = (a+dy, b+dx) with dy > 0, or dy == 0 and dx >= 0
+  for (int e = threadIdx.x; e < d * A.l1 * (2 * A.l2 - 1); e += blockDim.x) {
+    const int i = e / (A.l1 * (2 * A.l2 - 1));
+    const int rem = e % (A.l1 * (2 * A.l2 - 1));
+    const int dy = rem / (2 * A.l2 - 1);
+    const int dx = rem % (2 * A.l2 - 1) - (A.l2 - 1);
+    const int a = i / A.l2, b = i % A.l2;
+    const int a2 = a + dy, b2 = b + dx;
+    if (a2 >= A.l1 || b2 < 0 || b2 >= A.l2) continue;
+    if (dy == 0 && dx < 0) continue;
+    const int lag = dy * A.NDX + (dx + A.l2 - 1);
+    double s = 0.0;
+    for (int rz = 0; rz < A.nrz; ++rz) {
+      if (a < A.rz_lo[rz] || a > A.rz_hi[rz]) continue;
+      for (int cz = 0; cz < A.ncz; ++cz) {
+        if (b < A.cz_lo[cz] || b > A.cz_hi[cz]) continue;
+        s += Z[((int64_t)rz * A.ncz + cz) * A.NDF + lag];
+      }
+    }
+    const int j = a2 * A.l2 + b2;
+    C[i * d + j] = s;
+    C[j * d + i] = s;
+  }
+  __syncthreads();
+  double* out = A.payload + (int64_t)batch * A.plen + (view == 0 ? 0 : (int64_t)d * d);
+  if (!A.center) {
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) out[e] = C[e];
+    return;
+  }
+  // H C H with H = I - 11^T/d: C_ij - r_i/d - r_j/d + T/d^2 (C symmetric)
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    double r = 0.0;
+    for (int j = 0; j < d; ++j) r += C[i * d + j];
+    rs[i] = r;
+  }
+  __syncthreads();
+  __shared__ double tot;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < d; ++i) t += rs[i];
+    tot = t;
+  }
+  __syncthreads();
+  const double invd = 1.0 / d;
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    const int i = e / d, j = e % d;
+    out[e] = C[e] - rs[i] * invd - rs[j] * invd + tot * invd * invd;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// rect_sums: per-map window sums  sum_{patches} x  (centered if `center`)
+// ----------------------------------------------------------------------------
+struct RectArgs {
+  const float* maps[2];
+  double* out;  // [view][map][d]
+  const int* rz_of_y; const int* cz_of_x;
+  const int* rz_lo; const int* rz_hi; const int* cz_lo; const int* cz_hi;
+  int64_t n_maps;
+  int p, q, top, left, Hp, Wp, nrz, ncz, l1, l2, d, center;
+};
+
+__global__ void rect_sums_kernel(RectArgs A) {
+  extern __shared__ double sm[];
+  double* rowz = sm;                          // [Hp][ncz]
+  double* Zp = sm + (int64_t)A.Hp * A.ncz;    // [nrz][ncz]
+  double* R = Zp + A.nrz * A.ncz;             // [d]
+  const int64_t m = blockIdx.x;
+  const int view = blockIdx.y;
+  const float* img = (view == 0 ? A.maps[0] : A.maps[1]) + m * (int64_t)A.p * A.q;
+  for (int e = threadIdx.x; e < A.Hp * A.ncz; e += blockDim.x) rowz[e] = 0.0;
+  __syncthreads();
+  // one thread per padded row: column-zone sums of that row (pads are zero)
+  for (int y = threadIdx.x; y < A.Hp; y += blockDim.x) {
+    const int i = y - A.top;
+    if (i < 0 || i >= A.p) continue;
+    double cur = 0.0;
+    int czc = A.cz_of_x[A.left];
+    for (int j = 0; j < A.q; ++j) {
+      const int cz = A.cz_of_x[j + A.left];
+      if (cz != czc) {
+        rowz[y * A.ncz + czc] += cur;
+        cur = 0.0;
+        czc = cz;
+      }
+      cur += (double)img[(int64_t)i * A.q + j];
+    }
+    rowz[y * A.ncz + czc] += cur;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < A.nrz * A.ncz; e += blockDim.x) {
+    const int rz = e / A.ncz, cz = e % A.ncz;
+    double s = 0.0;
+    for (int y = 0; y < A.Hp; ++y)
+      if (A.rz_of_y[y] == rz) s += rowz[y * A.ncz + cz];
+    Zp[e] = s;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < A.d; k += blockDim.x) {
+    const int a = k / A.l2, b = k % A.l2;
+    double s = 0.0;
+    for (int rz = 0; rz < A.nrz; ++rz) {
+      if (a < A.rz_lo[rz] || a > A.rz_hi[rz]) continue;
+      for (int cz = 0; cz < A.ncz; ++cz)
+        if (b >= A.cz_lo[cz] && b <= A.cz_hi[cz]) s += Zp[rz * A.ncz + cz];
+    }
+    R[k] = s;
+  }
+  __syncthreads();
+  __shared__ double mean;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < A.d; ++k) t += R[k];
+    mean = t / A.d;
+  }
+  __syncthreads();
+  double* o = A.out + ((int64_t)view * A.n_maps + m) * A.d;
+  for (int k = threadIdx.x; k < A.d; k += blockDim.x) o[k] = A.center ? R[k] - mean : R[k];
+}
+
+// ----------------------------------------------------------------------------
+// batch_epilogue: class sums S (d x C), global sums g, counts
+// ----------------------------------------------------------------------------
+__global__ void batch_epilogue_kernel(const double* __restrict__ msum, const int32_t* __restrict__ label,
+                                      const int64_t* __restrict__ batch_off, int64_t n_maps, int d, int C,
+                                      int64_t plen, double cols_per_map, double* __restrict__ payload) {
+  const int batch = blockIdx.x;
+  const int view = blockIdx.y;
+  const PayloadView pv = payload_view(d, C);
+  double* P = payload + (int64_t)batch * plen;
+  double* S = P + (view == 0 ? pv.s1 : pv.s2);
+  double* g = P + (view == 0 ? pv.g1 : pv.g2);
+  const int64_t m0 = batch_off[batch], m1 = batch_off[batch + 1];
+  for (int e = threadIdx.x; e < d * C; e += blockDim.x) S[e] = 0.0;
+  __syncthreads();
+  const double* src = msum + (int64_t)view * n_maps * d;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    double gs = 0.0;
+    for (int64_t m = m0; m < m1; ++m) {
+      const double v = src[m * d + k];
+      S[(int64_t)k * C + label[m]] += v;
+      gs += v;
+    }
+    g[k] = gs;
+  }
+  if (view == 0) {
+    double* cnt = P + pv.ncls;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) cnt[c] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int64_t m = m0; m < m1; ++m) cnt[label[m]] += cols_per_map;
+      P[pv.n] = (double)(m1 - m0) * cols_per_map;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// direct path (any stride / padding): explicit float64 patches per block
+// ----------------------------------------------------------------------------
+constexpr int DIRECT_K = 64;  // patches staged per step
+constexpr int DIRECT_ENT = 8; // Gram entries per thread per pass
+
+__global__ void direct_gram_kernel(const float* maps1, const float* maps2, const int64_t* batch_off, Geo g,
+                                   int center, int nsplit, double* rec /* [batch][view][split][d*d] */) {
+  extern __shared__ double stage[];  // [DIRECT_K][d]
+  const int split = blockIdx.x;
+  const int batch = blockIdx.y;
+  const int view = blockIdx.z;
+  const float* src = view == 0 ? maps1 : maps2;
+  const int d = g.d;
+  const int64_t m0 = batch_off[batch], m1 = batch_off[batch + 1];
+  const int64_t cols_per_map = (int64_t)g.oh * g.ow;
+  const int64_t ncols = (m1 - m0) * cols_per_map;
+  const int64_t per = (ncols + nsplit - 1) / nsplit;
+  const int64_t c0 = (int64_t)split * per, c1 = min(ncols, c0 + per);
+  const int nent = d * d;
+  double* out = rec + (((int64_t)batch * 2 + view) * nsplit + split) * nent;
+  // entries are processed in passes of DIRECT_ENT * blockDim; patches are restaged per pass
+  for (int e0 = 0; e0 < nent; e0 += DIRECT_ENT * blockDim.x) {
+    double acc[DIRECT_ENT];
+#pragma unroll
+    for (int u = 0; u < DIRECT_ENT; ++u) acc[u] = 0.0;
+    for (int64_t cb = c0; cb < c1; cb += DIRECT_K) {
+      const int kk = (int)min((int64_t)DIRECT_K, c1 - cb);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kk * d; e += blockDim.x) {
+        const int k = e / d, t = e % d;
+        const int64_t col = cb + k;
+        const int64_t m = m0 + col / cols_per_map;
+        const int pos = (int)(col % cols_per_map);
+        const int u = pos / g.ow, v = pos % g.ow;
+        const int i = u * g.stride - g.top + t / g.l2, j = v * g.stride - g.left + t % g.l2;
+        float x = 0.f;
+        if (i >= 0 && i < g.p && j >= 0 && j < g.q) x = src[m * (int64_t)g.p * g.q + (int64_t)i * g.q + j];
+        stage[k * d + t] = (double)x;
+      }
+      __syncthreads();
+      if (center) {
+        for (int k = threadIdx.x; k < kk; k += blockDim.x) {
+          double s = 0.0;
+          for (int t = 0; t < d; ++t) s += stage[k * d + t];
+          const double mu = s / d;
+          for (int t = 0; t < d; ++t) stage[k * d + t] -= mu;
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < DIRECT_ENT; ++u) {
+        const int e = e0 + threadIdx.x + u * blockDim.x;
+        if (e < nent) {
+          const int i = e / d, j = e % d;
+          double s = acc[u];
+          for (int k = 0; k < kk; ++k) s = fma(stage[k * d + i], stage[k * d + j], s);
+          acc[u] = s;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DIRECT_ENT; ++u) {
+      const int e = e0 + threadIdx.x + u * blockDim.x;
+      if (e < nent) out[e] = acc[u];
+    }
+  }
+}
+
+__global__ void direct_reduce_kernel(const double* rec, int nsplit, int d, int64_t plen, double* payload) {
+  const int bv = blockIdx.x;
+  const int batch = bv >> 1, view = bv & 1;
+  const int nent = d * d;
+  double* out = payload + (int64_t)batch * plen + (view == 0 ? 0 : nent);
+  for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) s += rec[((int64_t)bv * nsplit + sp) * nent + e];
+    out[e] = s;
+  }
+}
+
+// per-map patch sums for the direct path (any stride): sum over the patch grid
+__global__ void direct_map_sums_kernel(const float* maps1, const float* maps2, int64_t n_maps, Geo g, int center,
+                                       double* out /* [view][map][d] */) {
+  extern __shared__ double R[];
+  const int64_t m = blockIdx.x;
+  const int view = blockIdx.y;
+  const float* img = (view == 0 ? maps1 : maps2) + m * (int64_t)g.p * g.q;
+  const int d = g.d;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    const int di = t / g.l2, dj = t % g.l2;
+    double s = 0.0;
+    for (int u = 0; u < g.oh; ++u) {
+      const int i = u * g.stride - g.top + di;
+      if (i < 0 || i >= g.p) continue;
+      for (int v = 0; v < g.ow; ++v) {
+        const int j = v * g.stride - g.left + dj;
+        if (j >= 0 && j < g.q) s += (double)img[(int64_t)i * g.q + j];
+      }
+    }
+    R[t] = s;
+  }
+  __syncthreads();
+  __shared__ double mean;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < d; ++k) t += R[k];
+    mean = t / d;
+  }
+  __syncthreads();
+  double* o = out + ((int64_t)view * n_maps + m) * d;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) o[k] = center ? R[k] - mean : R[k];
+}
+
+// ----------------------------------------------------------------------------
+// explicit columns (API accumulate_batch): per-block partial Gram + class sums
+// ----------------------------------------------------------------------------
+constexpr int COLS_PER_BLOCK = 2048;
+
+__global__ void columns_partial_kernel(const double* x, const double* y, const int64_t* labels, int64_t cols, int d,
+                                       int C, double* part /* [block][view][d*d + d*C + d] */) {
+  extern __shared__ double st[];  // [DIRECT_K][d] x2
+  const int64_t c0 = (int64_t)blockIdx.x * COLS_PER_BLOCK;
+  const int64_t c1 = min(cols, c0 + COLS_PER_BLOCK);
+  const int nent = d * d;
+  const int64_t per_view = (int64_t)nent + (int64_t)d * C + d;
+  double* outb = part + (int64_t)blockIdx.x * 2 * per_view;
+  for (int view = 0; view < 2; ++view) {
+    const double* src = view == 0 ? x : y;
+    double* o = outb + view * per_view;
+    // Gram entries
+    for (int e0 = 0; e0 < nent; e0 += blockDim.x) {
+      const int e = e0 + threadIdx.x;
+      double s = 0.0;
+      for (int64_t cb = c0; cb < c1; cb += DIRECT_K) {
+        const int kk = (int)min((int64_t)DIRECT_K, c1 - cb);
+        __syncthreads();
+        for (int t = threadIdx.x; t < kk * d; t += blockDim.x) {
+          const int k = t / d, r = t % d;
+          st[k * d + r] = src[(int64_t)r * cols + cb + k];
+        }
+        __syncthreads();
+        if (e < nent) {
+          const int i = e / d, j = e % d;
+          for (int k = 0; k < kk; ++k) s = fma(st[k * d + i], st[k * d + j], s);
+        }
+      }
+      if (e < nent) o[e] = s;
+    }
+    // class sums and global sums (thread per row, columns in order)
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+      double* S = o + nent;
+      for (int c = 0; c < C; ++c) S[(int64_t)k * C + c] = 0.0;
+      double gs = 0.0;
+      for (int64_t c = c0; c < c1; ++c) {
+        const double v = src[(int64_t)k * cols + c];
+        S[(int64_t)k * C + labels[c]] += v;
+        gs += v;
+      }
+      o[nent + (int64_t)d * C + k] = gs;
+    }
+  }
+}
+
+__global__ void columns_reduce_kernel(const double* part, int nblk, const int64_t* labels, int64_t cols, int d,
+                                      int C, double* payload) {
+  const PayloadView pv = payload_view(d, C);
+  const int nent = d * d;
+  const int64_t per_view = (int64_t)nent + (int64_t)d * C + d;
+  for (int view = 0; view < 2; ++view) {
+    for (int64_t e = threadIdx.x; e < per_view; e += blockDim.x) {
+      double s = 0.0;
+      for (int b = 0; b < nblk; ++b) s += part[((int64_t)b * 2 + view) * per_view + e];
+      int64_t dst;
+      if (e < nent) dst = (view == 0 ? pv.c11 : pv.c22) + e;
+      else if (e < nent + (int64_t)d * C) dst = (view == 0 ? pv.s1 : pv.s2) + (e - nent);
+      else dst = (view == 0 ? pv.g1 : pv.g2) + (e - nent - (int64_t)d * C);
+      payload[dst] += s;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int64_t c = 0; c < cols; ++c) payload[pv.ncls + labels[c]] += 1.0;
+    payload[pv.n] += (double)cols;
+  }
+}
+
+__global__ void tree_level_kernel(double* parts, int n, int64_t len, int stride_in) {
+  // pairs (i, i+1) at positions i = 0, 2, ... in the current level; level entries are
+  // spaced `stride_in` payloads apart. Result stored in place of the left element.
+  const int npairs = n / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)npairs * len;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int pr = (int)(e / len);
+    const int64_t k = e % len;
+    double* a = parts + (int64_t)(2 * pr) * stride_in * len;
+    const double* b = parts + (int64_t)(2 * pr + 1) * stride_in * len;
+    a[k] = a[k] + b[k];
+  }
+}
+
+}  // namespace ddcca
+
+using namespace ddcca;
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+namespace {
+
+struct LagLayout {
+  Plan P;
+  int nsplit;
+  size_t off_tasks, off_lane, off_boff, off_rec, off_Z, off_zoff, off_zlist, off_zones, off_msum, total;
+  int nzone_rec;  // total entries of zrec_list
+};
+
+static int nsplit_for(int64_t max_maps) {
+  int64_t s = (max_maps + MAPS_PER_SPLIT - 1) / MAPS_PER_SPLIT;
+  return (int)std::max<int64_t>(1, s);
+}
+
+static void lag_layout(const Geo& g, int nb, int64_t max_maps, int64_t n_maps, LagLayout* L) {
+  make_plan(g, &L->P);
+  L->nsplit = nsplit_for(max_maps);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+  L->off_tasks = take(sizeof(TaskDev) * L->P.tasks.size());
+  L->off_lane = take(sizeof(int) * L->P.lane_slot.size());
+  L->off_boff = take(sizeof(int64_t) * (nb + 1));
+  L->off_rec = take(sizeof(double) * (size_t)nb * 2 * L->nsplit * L->P.nrec * L->P.NDF);
+  L->off_Z = take(sizeof(double) * (size_t)nb * 2 * L->P.nrz * L->P.ncz * L->P.NDF);
+  L->off_zoff = take(sizeof(int) * (L->P.nrz * L->P.ncz + 1));
+  L->off_zlist = take(sizeof(int) * L->P.nrec);
+  L->off_zones = take(sizeof(int) * (2 * L->P.nrz + 2 * L->P.ncz + g.Hp + g.Wp));
+  L->off_msum = take(sizeof(double) * 2 * (size_t)n_maps * g.d);
+  L->total = o;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ddcca_version(void) { return 1; }
+
+const char* ddcca_last_error(void) { return err_buf(); }
+
+int64_t ddcca_payload_len(int dim, int class_count) { return payload_len(dim, class_count); }
+
+size_t ddcca_moments_workspace(const ddcca_geom* gg, int n_batches, int64_t max_maps_per_batch, int class_count) {
+  (void)class_count;
+  Geo g;
+  if (make_geo(gg, &g) != DDCCA_OK) return 0;
+  // worst case over the per-batch maps: n_maps <= n_batches * max_maps
+  const int64_t n_maps = (int64_t)n_batches * max_maps_per_batch;
+  if (g.stride == 1 && g.l1 <= MAX_LAG_L && g.l2 <= MAX_LAG_L) {
+    LagLayout L;
+    lag_layout(g, n_batches, max_maps_per_batch, n_maps, &L);
+    return L.total;
+  }
+  const int nsplit = nsplit_for(max_maps_per_batch);
+  return align_up(sizeof(double) * (size_t)n_batches * 2 * nsplit * g.d * g.d, 256) +
+         align_up(sizeof(int64_t) * (n_batches + 1), 256) + align_up(sizeof(double) * 2 * (size_t)n_maps * g.d, 256);
+}
+
+int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t* map_label,
+                          const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* gg, int center,
+                          int class_count, double* partials, void* ws, size_t ws_bytes, void* stream) {
+  Geo g;
+  DDCCA_TRY(make_geo(gg, &g));
+  if (n_batches < 1) return fail(DDCCA_ECONFIG, "no batches to accumulate");
+  if (class_count < 1) return fail(DDCCA_ECONFIG, "invalid class count %d", class_count);
+  if (!maps1 || !maps2 || !map_label || !partials || !batch_offsets_host) return fail(DDCCA_ESHAPE, "null pointer");
+  int64_t max_maps = 0;
+  for (int b = 0; b < n_batches; ++b) {
+    const int64_t n = batch_offsets_host[b + 1] - batch_offsets_host[b];
+    if (n < 1) return fail(DDCCA_ESHAPE, "batch %d is empty", b);
+    max_maps = std::max(max_maps, n);
+  }
+  const int64_t n_maps = batch_offsets_host[n_batches];
+  if (batch_offsets_host[0] != 0) return fail(DDCCA_ESHAPE, "batch offsets must start at 0");
+  cudaStream_t st = as_stream(stream);
+  const int64_t plen = payload_len(g.d, class_count);
+  const double cols_per_map = (double)g.oh * g.ow;
+  char* w = static_cast<char*>(ws);
+
+  if (g.stride == 1 && g.l1 <= MAX_LAG_L && g.l2 <= MAX_LAG_L) {
+    LagLayout L;
+    lag_layout(g, n_batches, max_maps, n_maps, &L);
+    if (ws_bytes < L.total) return fail(DDCCA_ECONFIG, "moments workspace too small (%zu < %zu)", ws_bytes, L.total);
+    const Plan& P = L.P;
+    // upload plan tables (small; pageable H2D copies are staged by the driver)
+    std::vector<TaskDev> td(P.tasks.size());
+    for (size_t t = 0; t < P.tasks.size(); ++t) td[t] = {P.tasks[t].y0, P.tasks[t].y1, P.tasks[t].x0, P.tasks[t].rec0};
+    const int nzone = P.nrz * P.ncz;
+    std::vector<int> zoff(nzone + 1, 0), zlist(P.nrec);
+    for (int r = 0; r < P.nrec; ++r) zoff[P.recs[r].rz * P.ncz + P.recs[r].cz + 1]++;
+    for (int z = 0; z < nzone; ++z) zoff[z + 1] += zoff[z];
+    {
+      std::vector<int> fill(zoff.begin(), zoff.end() - 1);
+      for (int r = 0; r < P.nrec; ++r) zlist[fill[P.recs[r].rz * P.ncz + P.recs[r].cz]++] = r;
+    }
+    std::vector<int> zones;
+    zones.insert(zones.end(), P.z.rz_lo.begin(), P.z.rz_lo.end());
+    zones.insert(zones.end(), P.z.rz_hi.begin(), P.z.rz_hi.end());
+    zones.insert(zones.end(), P.z.cz_lo.begin(), P.z.cz_lo.end());
+    zones.insert(zones.end(), P.z.cz_hi.begin(), P.z.cz_hi.end());
+    zones.insert(zones.end(), P.z.rz_of_y.begin(), P.z.rz_of_y.end());
+    zones.insert(zones.end(), P.z.cz_of_x.begin(), P.z.cz_of_x.end());
+    cudaMemcpyAsync(w + L.off_tasks, td.data(), sizeof(TaskDev) * td.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(w + L.off_lane, P.lane_slot.data(), sizeof(int) * P.lane_slot.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(w + L.off_boff, batch_offsets_host, sizeof(int64_t) * (n_batches + 1), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(w + L.off_zoff, zoff.data(), sizeof(int) * zoff.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(w + L.off_zlist, zlist.data(), sizeof(int) * zlist.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(w + L.off_zones, zones.data(), sizeof(int) * zones.size(), cudaMemcpyHostToDevice, st);
+    DDCCA_TRY(check_launch("moments: plan upload"));
+    const int* zd = reinterpret_cast<const int*>(w + L.off_zones);
+    const int *rz_lo = zd, *rz_hi = zd + P.nrz, *cz_lo = zd + 2 * P.nrz, *cz_hi = zd + 2 * P.nrz + P.ncz;
+    const int* rz_of_y = zd + 2 * P.nrz + 2 * P.ncz;
+    const int* cz_of_x = rz_of_y + g.Hp;
+
+    LagArgs A;
+    A.maps[0] = maps1;
+    A.maps[1] = maps2;
+    A.tasks = reinterpret_cast<const TaskDev*>(w + L.off_tasks);
+    A.lane_slot = reinterpret_cast<const int*>(w + L.off_lane);
+    A.batch_off = reinterpret_cast<const int64_t*>(w + L.off_boff);
+    A.rec = reinterpret_cast<double*>(w + L.off_rec);
+    A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
+    A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.nbatch = n_batches;
+    const int maxrows = SLAB_Y + g.l1 - 1;
+    const size_t smem = sizeof(double) * maxrows * (TILE_X + P.NDX - 1);
+    dim3 grid((unsigned)P.tasks.size(), (unsigned)L.nsplit, (unsigned)(n_batches * 2));
+    dim3 block(32 * P.G);
+    switch (g.l1) {
+#define DDCCA_LAG_CASE(N)                                                                          \
+  case N:                                                                                          \
+    cudaFuncSetAttribute(lag_zone_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    lag_zone_kernel<N><<<grid, block, smem, st>>>(A);                                              \
+    break;
+      DDCCA_LAG_CASE(1) DDCCA_LAG_CASE(2) DDCCA_LAG_CASE(3) DDCCA_LAG_CASE(4) DDCCA_LAG_CASE(5)
+      DDCCA_LAG_CASE(6) DDCCA_LAG_CASE(7) DDCCA_LAG_CASE(8) DDCCA_LAG_CASE(9) DDCCA_LAG_CASE(10)
+      DDCCA_LAG_CASE(11) DDCCA_LAG_CASE(12)
+#undef DDCCA_LAG_CASE
+      default:
+        return fail(DDCCA_ECONFIG, "unsupported window height %d", g.l1);
+    }
+    DDCCA_TRY(check_launch("moments: lag_zone_kernel"));
+    double* Z = reinterpret_cast<double*>(w + L.off_Z);
+    {
+      dim3 gz((unsigned)std::min<int64_t>(64, ((int64_t)nzone * P.NDF + 255) / 256), (unsigned)(n_batches * 2));
+      zone_reduce_kernel<<<gz, 256, 0, st>>>(A.rec, reinterpret_cast<const int*>(w + L.off_zoff),
+                                             reinterpret_cast<const int*>(w + L.off_zlist), Z, nzone, P.NDF, P.nrec,
+                                             L.nsplit);
+      DDCCA_TRY(check_launch("moments: zone_reduce"));
+    }
+    {
+      AsmArgs S;
+      S.Z = Z; S.rz_lo = rz_lo; S.rz_hi = rz_hi; S.cz_lo = cz_lo; S.cz_hi = cz_hi;
+      S.payload = partials; S.plen = plen; S.nrz = P.nrz; S.ncz = P.ncz; S.NDX = P.NDX; S.NDF = P.NDF;
+      S.l1 = g.l1; S.l2 = g.l2; S.d = g.d; S.center = center;
+      const size_t sm = sizeof(double) * ((size_t)g.d * g.d + g.d);
+      cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      assemble_kernel<<<n_batches * 2, 256, sm, st>>>(S);
+      DDCCA_TRY(check_launch("moments: assemble"));
+    }
+    {
+      RectArgs R;
+      R.maps[0] = maps1; R.maps[1] = maps2;
+      R.out = reinterpret_cast<double*>(w + L.off_msum);
+      R.rz_of_y = rz_of_y; R.cz_of_x = cz_of_x; R.rz_lo = rz_lo; R.rz_hi = rz_hi; R.cz_lo = cz_lo; R.cz_hi = cz_hi;
+      R.n_maps = n_maps; R.p = g.p; R.q = g.q; R.top = g.top; R.left = g.left; R.Hp = g.Hp; R.Wp = g.Wp;
+      R.nrz = P.nrz; R.ncz = P.ncz; R.l1 = g.l1; R.l2 = g.l2; R.d = g.d; R.center = center;
+      const size_t sm = sizeof(double) * ((size_t)g.Hp * P.ncz + (size_t)P.nrz * P.ncz + g.d);
+      cudaFuncSetAttribute(rect_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      rect_sums_kernel<<<dim3((unsigned)n_maps, 2), 128, sm, st>>>(R);
+      DDCCA_TRY(check_launch("moments: rect_sums"));
+      batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(R.out, map_label, A.batch_off, n_maps, g.d,
+                                                                 class_count, plen, cols_per_map, partials);
+      DDCCA_TRY(check_launch("moments: batch_epilogue"));
+    }
+    return DDCCA_OK;
+  }
+
+  // direct float64 path for stride != 1 (or very tall windows)
+  const int nsplit = nsplit_for(max_maps);
+  size_t o_rec = 0;
+  size_t o_boff = align_up(sizeof(double) * (size_t)n_batches * 2 * nsplit * g.d * g.d, 256);
+  size_t o_msum = o_boff + align_up(sizeof(int64_t) * (n_batches + 1), 256);
+  size_t need = o_msum + align_up(sizeof(double) * 2 * (size_t)n_maps * g.d, 256);
+  if (ws_bytes < need) return fail(DDCCA_ECONFIG, "moments workspace too small (%zu < %zu)", ws_bytes, need);
+  double* rec = reinterpret_cast<double*>(w + o_rec);
+  int64_t* boff = reinterpret_cast<int64_t*>(w + o_boff);
+  double* msum = reinterpret_cast<double*>(w + o_msum);
+  cudaMemcpyAsync(boff, batch_offsets_host, sizeof(int64_t) * (n_batches + 1), cudaMemcpyHostToDevice, st);
+  const size_t sm = sizeof(double) * DIRECT_K * g.d;
+  cudaFuncSetAttribute(direct_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  direct_gram_kernel<<<dim3(nsplit, n_batches, 2), 256, sm, st>>>(maps1, maps2, boff, g, center, nsplit, rec);
+  DDCCA_TRY(check_launch("moments: direct_gram"));
+  direct_reduce_kernel<<<n_batches * 2, 256, 0, st>>>(rec, nsplit, g.d, plen, partials);
+  DDCCA_TRY(check_launch("moments: direct_reduce"));
+  direct_map_sums_kernel<<<dim3((unsigned)n_maps, 2), 128, sizeof(double) * g.d, st>>>(maps1, maps2, n_maps, g, center,
+                                                                                      msum);
+  DDCCA_TRY(check_launch("moments: direct_map_sums"));
+  batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(msum, map_label, boff, n_maps, g.d, class_count, plen,
+                                                             cols_per_map, partials);
+  return check_launch("moments: batch_epilogue");
+}
+
+int ddcca_moments_tree(double* parts, int n_parts, int64_t payload_len_, double* out, void* stream) {
+  if (n_parts < 1) return fail(DDCCA_ECONFIG, "nothing to merge");
+  cudaStream_t st = as_stream(stream);
+  // Level k combines entries spaced 2^k apart; an odd tail is carried unchanged,
+  // which is exactly the left-to-right tree of pairwise_merge (moments.py:132-144).
+  int n = n_parts, stride = 1;
+  while (n > 1) {
+    const int npairs = n / 2;
+    const int64_t work = (int64_t)npairs * payload_len_;
+    const int blocks = (int)std::min<int64_t>(4096, (work + 255) / 256);
+    tree_level_kernel<<<blocks, 256, 0, st>>>(parts, n, payload_len_, stride);
+    DDCCA_TRY(check_launch("moments: tree level"));
+    // carried tail: element n-1 (odd) moves to position npairs in the next level,
+    // i.e. index (n-1)*stride stays where it is and next level stride doubles;
+    // with the in-place scheme next-level entry j lives at j * 2*stride, and the
+    // tail at (n-1)*stride == npairs * 2*stride, so nothing needs to move.
+    n = (n + 1) / 2;
+    stride *= 2;
+  }
+  if (out != parts)
+    cudaMemcpyAsync(out, parts, sizeof(double) * payload_len_, cudaMemcpyDeviceToDevice, st);
+  return check_launch("moments: tree copy");
+}
+
+int ddcca_accumulate_columns(const double* x, const double* y, const int64_t* labels, int64_t cols, int dim,
+                             int class_count, double* payload, void* stream) {
+  if (dim < 1 || class_count < 1) return fail(DDCCA_ECONFIG, "invalid accumulator shape dim=%d classes=%d", dim, class_count);
+  if (cols < 0) return fail(DDCCA_ESHAPE, "negative column count");
+  if (cols == 0) return DDCCA_OK;
+  if (dim * dim > 1 << 16) return fail(DDCCA_ECONFIG, "dim %d too large", dim);
+  cudaStream_t st = as_stream(stream);
+  const int nblk = (int)((cols + COLS_PER_BLOCK - 1) / COLS_PER_BLOCK);
+  const int64_t per_view = (int64_t)dim * dim + (int64_t)dim * class_count + dim;
+  double* part = nullptr;
+  if (cudaMallocAsync(&part, sizeof(double) * (size_t)nblk * 2 * per_view, st) != cudaSuccess)
+    return fail(DDCCA_ECUDA, "accumulate_columns: out of memory");
+  const size_t sm = sizeof(double) * DIRECT_K * dim;
+  cudaFuncSetAttribute(columns_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  columns_partial_kernel<<<nblk, 256, sm, st>>>(x, y, labels, cols, dim, class_count, part);
+  int rc = check_launch("accumulate_columns: partial");
+  if (rc == DDCCA_OK) {
+    columns_reduce_kernel<<<1, 256, 0, st>>>(part, nblk, labels, cols, dim, class_count, payload);
+    rc = check_launch("accumulate_columns: reduce");
+  }
+  cudaFreeAsync(part, st);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,634 @@
+// K4+K5: finalize + DCCA filter solve on device, one CTA, float64.
+//
+// Restates moments.finalize (moments.py:168-193) and solver.solve_dcca /
+// sym_eig / inv_sqrt / reshape_filters (solver.py:32-272) including the
+// reference's ordering semantics: cyclic Jacobi with the round-robin pair
+// schedule (solver.py:32-46), unit-Frobenius pre-scaling, 1e-12 off-diagonal
+// stop, 100-sweep cap, stable descending sort, largest-|entry|-positive sign
+// rule (solver.py:49-57), lexicographic order inside near-degenerate runs
+// (solver.py:60-79), and null-space completion for sigma <= 1e-12 sigma_1
+// (solver.py:238-247). The problem is d x d with d = l1*l2 <= ~100, so one
+// CTA with the Jacobi matrices in shared memory is the right shape: the
+// solve is latency-bound (a few hundred rotation rounds), not FLOP-bound.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ddcca {
+
+constexpr int SOLVE_THREADS = 512;
+constexpr int SMEM_JACOBI_MAX_N = 110;  // 2*n*n doubles in shared memory
+
+struct Blk {
+  double* red;   // reduction scratch, SOLVE_THREADS doubles (shared)
+  int* flag;     // shared error flag
+  int* iscr;     // shared int scratch, >= 2*n ints
+};
+
+__device__ double block_sum(double v, Blk& B) {
+  const int t = threadIdx.x;
+  v = warp_sum(v);
+  __syncthreads();
+  if ((t & 31) == 0) B.red[t >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (t < 32) {
+    s = (t < (int)(blockDim.x >> 5)) ? B.red[t] : 0.0;
+    s = warp_sum(s);
+    if (t == 0) B.red[0] = s;
+  }
+  __syncthreads();
+  s = B.red[0];
+  __syncthreads();
+  return s;
+}
+
+__device__ double block_max(double v, Blk& B) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((t & 31) == 0) B.red[t >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (t < 32) {
+    s = (t < (int)(blockDim.x >> 5)) ? B.red[t] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (t == 0) B.red[0] = s;
+  }
+  __syncthreads();
+  s = B.red[0];
+  __syncthreads();
+  return s;
+}
+
+__device__ double offdiag_norm(const double* a, int n, Blk& B) {
+  double s = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    if (i != j) s += a[e] * a[e];
+  }
+  return sqrt(block_sum(s, B));
+}
+
+// seat of position k in round r of the round-robin tournament (solver.py:32-46)
+__device__ __forceinline__ int rr_seat(int k, int r, int m) {
+  if (k == 0) return 0;
+  int v = (k - 1 - r) % (m - 1);
+  if (v < 0) v += m - 1;
+  return v + 1;
+}
+
+// argsort(-w, kind="stable"): rank of element i
+__device__ __forceinline__ int desc_rank(const double* w, int n, int i) {
+  const double wi = w[i];
+  int r = 0;
+  for (int j = 0; j < n; ++j) {
+    const double wj = w[j];
+    if (wj > wi || (wj == wi && j < i)) ++r;
+  }
+  return r;
+}
+
+// Sign per column: largest |entry| (first on ties) made positive (solver.py:49-57).
+__device__ void col_signs(const double* v, int n, int ncols, int ld, double* sgn) {
+  for (int j = threadIdx.x; j < ncols; j += blockDim.x) {
+    int best = 0;
+    double bv = fabs(v[j]);
+    for (int i = 1; i < n; ++i) {
+      const double x = fabs(v[i * ld + j]);
+      if (x > bv) { bv = x; best = i; }
+    }
+    const double e = v[best * ld + j];
+    sgn[j] = e > 0.0 ? 1.0 : (e < 0.0 ? -1.0 : 1.0);
+  }
+}
+
+// Lexicographic comparison of columns i and j of v (n rows, leading dim ld).
+__device__ __forceinline__ int lex_cmp(const double* v, int n, int ld, int i, int j) {
+  for (int k = 0; k < n; ++k) {
+    const double a = v[k * ld + i], b = v[k * ld + j];
+    if (a < b) return -1;
+    if (a > b) return 1;
+  }
+  return 0;
+}
+
+// Symmetric eigensolver (solver.py:90-158). s: input n x n (global). Results:
+// w (n), v (n x n row-major, column j = eigenvector j). a, tmp: n*n scratch
+// (shared or global). Returns DDCCA_* status (uniform across the block).
+__device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double* a, double* tmp, double* wtmp,
+                           Blk& B) {
+  const int nn = n * n;
+  double mx = 0.0;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) mx = fmax(mx, fabs(s[e]));
+  mx = block_max(mx, B);
+  // identity start
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) v[e] = (e / n == e % n) ? 1.0 : 0.0;
+  if (n == 1 || mx == 0.0) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) wtmp[i] = s[i * n + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int r = desc_rank(wtmp, n, i);
+      w[r] = wtmp[i];
+      for (int k = 0; k < n; ++k) v[k * n + r] = (k == i) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    return DDCCA_OK;
+  }
+  // unit-scaled copy, its Frobenius norm and the symmetry test
+  double fs = 0.0, as = 0.0;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    const double u = s[e] / mx, ut = s[j * n + i] / mx;
+    fs += u * u;
+    as += (u - ut) * (u - ut);
+  }
+  const double fro_u = sqrt(block_sum(fs, B));
+  const double asym = sqrt(block_sum(as, B));
+  if (asym > 1e-10 * fro_u) return DDCCA_ESHAPE;
+  const double norm = mx * fro_u;
+  const double f = mx / norm;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    a[e] = 0.5 * (s[e] / mx + s[j * n + i] / mx) * f;
+  }
+  __syncthreads();
+  const int m = n + (n & 1);
+  const int npair = m / 2;
+  double* cs = wtmp;            // reuse: c in [0, npair), s in [npair, 2*npair) -> needs 2*npair <= n+1
+  int* pp = B.iscr;             // p of pair t
+  int* qq = B.iscr + npair;     // q of pair t (or -1 if inactive/dummy)
+  bool converged = false;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    if (offdiag_norm(a, n, B) <= 1e-12) { converged = true; break; }
+    for (int r = 0; r < m - 1; ++r) {
+      for (int t = threadIdx.x; t < npair; t += blockDim.x) {
+        const int u = rr_seat(t, r, m), x = rr_seat(m - 1 - t, r, m);
+        int p = min(u, x), q = max(u, x);
+        double c = 1.0, sn = 0.0;
+        if (q < n) {
+          const double apq = a[p * n + q];
+          if (apq != 0.0) {
+            const double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
+            const double sg = theta >= 0.0 ? 1.0 : -1.0;
+            const double tt = sg / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(tt * tt + 1.0);
+            sn = tt * c;
+          } else {
+            q = -1;
+          }
+        } else {
+          q = -1;
+        }
+        pp[t] = p;
+        qq[t] = q;
+        cs[2 * t] = c;
+        cs[2 * t + 1] = sn;
+      }
+      __syncthreads();
+      // rows: B = J^T a
+      for (int e = threadIdx.x; e < npair * n; e += blockDim.x) {
+        const int t = e / n, j = e - t * n;
+        const int q = qq[t];
+        if (q < 0) continue;
+        const int p = pp[t];
+        const double c = cs[2 * t], sn = cs[2 * t + 1];
+        const double ap = a[p * n + j], aq = a[q * n + j];
+        a[p * n + j] = c * ap - sn * aq;
+        a[q * n + j] = sn * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: a = B J, v = v J
+      for (int e = threadIdx.x; e < npair * n; e += blockDim.x) {
+        const int t = e / n, i = e - t * n;
+        const int q = qq[t];
+        if (q < 0) continue;
+        const int p = pp[t];
+        const double c = cs[2 * t], sn = cs[2 * t + 1];
+        const double bp = a[i * n + p], bq = a[i * n + q];
+        a[i * n + p] = c * bp - sn * bq;
+        a[i * n + q] = sn * bp + c * bq;
+        const double vp = v[i * n + p], vq = v[i * n + q];
+        v[i * n + p] = c * vp - sn * vq;
+        v[i * n + q] = sn * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    // a = (a + a^T) / 2
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      if (i < j) {
+        const double x = 0.5 * (a[e] + a[j * n + i]);
+        a[e] = x;
+        a[j * n + i] = x;
+      }
+    }
+    __syncthreads();
+  }
+  if (!converged && offdiag_norm(a, n, B) > 1e-12) return DDCCA_ENUMERICAL;
+  // eigenvalues, stable descending order
+  for (int i = threadIdx.x; i < n; i += blockDim.x) wtmp[i] = a[i * n + i] * norm;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = desc_rank(wtmp, n, i);
+    w[r] = wtmp[i];
+    for (int k = 0; k < n; ++k) tmp[k * n + r] = v[k * n + i];
+  }
+  __syncthreads();
+  // sign rule
+  col_signs(tmp, n, n, n, wtmp);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) tmp[e] *= wtmp[e % n];
+  __syncthreads();
+  // degenerate runs: |w[k] - w[start]| <= 1e-10 * max|w|, sorted lexicographically
+  int* run_start = B.iscr;  // n ints
+  if (threadIdx.x == 0) {
+    double sc = 0.0;
+    for (int i = 0; i < n; ++i) sc = fmax(sc, fabs(w[i]));
+    const double tol = 1e-10 * sc;
+    int start = 0;
+    for (int k = 1; k <= n; ++k) {
+      if (k < n && fabs(w[k] - w[start]) <= tol) continue;
+      for (int i = start; i < k; ++i) run_start[i] = start;
+      start = k;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int st = run_start[i];
+    int en = i + 1;
+    while (en < n && run_start[en] == st) ++en;
+    int r = st;
+    for (int j = st; j < en; ++j) {
+      if (j == i) continue;
+      const int c = lex_cmp(tmp, n, n, j, i);
+      if (c < 0 || (c == 0 && j < i)) ++r;
+    }
+    wtmp[r] = w[i];
+    for (int k = 0; k < n; ++k) v[k * n + r] = tmp[k * n + i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = wtmp[i];
+  __syncthreads();
+  return DDCCA_OK;
+}
+
+// C = op(A) * op(B) for n x n row-major matrices (ta/tb: use transpose)
+__device__ void matmul(const double* A, bool ta, const double* Bm, bool tb, double* C, int n, int kdim, int mcols) {
+  // C (n x mcols) = A' (n x kdim) * B' (kdim x mcols)
+  for (int e = threadIdx.x; e < n * mcols; e += blockDim.x) {
+    const int i = e / mcols, j = e - i * mcols;
+    double s = 0.0;
+    for (int k = 0; k < kdim; ++k) {
+      const double x = ta ? A[k * n + i] : A[i * kdim + k];
+      const double y = tb ? Bm[j * kdim + k] : Bm[k * mcols + j];
+      s += x * y;
+    }
+    C[e] = s;
+  }
+  __syncthreads();
+}
+
+// inv_sqrt (solver.py:161-170) into r; eigen scratch from the caller.
+__device__ int inv_sqrt_dev(const double* c, int n, double* r, double* w, double* v, double* a, double* tmp,
+                            double* wtmp, Blk& B) {
+  int rc = sym_eig_dev(c, n, w, v, a, tmp, wtmp, B);
+  if (rc != DDCCA_OK) return rc;
+  if (!(w[n - 1] > 0.0)) return DDCCA_ENUMERICAL;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += (v[i * n + k] * pow(w[k], -0.5)) * v[j * n + k];
+    tmp[e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    r[e] = 0.5 * (tmp[e] + tmp[j * n + i]);
+  }
+  __syncthreads();
+  return DDCCA_OK;
+}
+
+// finalize (moments.py:168-193): Cw = S1 S2^T, Cb = g1 g2^T - Cw, Ct = Cw - Cb,
+// C11 = sym(C11) + eps * tr/d * I (same for C22). Returns false on an empty
+// accumulator (NumericalError in the reference).
+__device__ bool finalize_dev(const double* P, int n, int C, double eps, double* fin, Blk& B) {
+  const PayloadView pv = payload_view(n, C);
+  const int nn = n * n;
+  double* c11 = fin;
+  double* c22 = fin + nn;
+  double* cw = fin + 2 * nn;
+  double* cb = fin + 3 * nn;
+  double* ct = fin + 4 * nn;
+  if (!(P[pv.n] >= 1.0)) return false;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    double s = 0.0;
+    for (int c = 0; c < C; ++c) s += P[pv.s1 + (int64_t)i * C + c] * P[pv.s2 + (int64_t)j * C + c];
+    cw[e] = s;
+    cb[e] = P[pv.g1 + i] * P[pv.g2 + j] - s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) ct[e] = cw[e] - cb[e];
+  double tr1 = 0.0, tr2 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    tr1 += 0.5 * (P[pv.c11 + i * n + i] + P[pv.c11 + i * n + i]);
+    tr2 += 0.5 * (P[pv.c22 + i * n + i] + P[pv.c22 + i * n + i]);
+  }
+  tr1 = block_sum(tr1, B);
+  tr2 = block_sum(tr2, B);
+  const double rid1 = eps * (tr1 / n), rid2 = eps * (tr2 / n);
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    c11[e] = 0.5 * (P[pv.c11 + e] + P[pv.c11 + j * n + i]) + (i == j ? rid1 : 0.0);
+    c22[e] = 0.5 * (P[pv.c22 + e] + P[pv.c22 + j * n + i]) + (i == j ? rid2 : 0.0);
+  }
+  __syncthreads();
+  return true;
+}
+
+__global__ void __launch_bounds__(SOLVE_THREADS) finalize_kernel(const double* P, int n, int C, double eps, double* fin,
+                                                                 int32_t* status) {
+  __shared__ double red[SOLVE_THREADS / 32 + 1];
+  __shared__ int flag;
+  __shared__ int iscr[2];
+  Blk B{red, &flag, iscr};
+  const bool ok = finalize_dev(P, n, C, eps, fin, B);
+  if (threadIdx.x == 0) *status = ok ? DDCCA_OK : DDCCA_ENUMERICAL;
+}
+
+struct SolveArgs {
+  const double* payload;
+  int d, C, count;
+  double eps;
+  double *fin, *w1, *w2, *rho;
+  float *pack1, *pack2;
+  int32_t* status;
+  double* ws;  // global scratch
+  int jacobi_in_smem;
+};
+
+__global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
+  extern __shared__ double sm[];
+  __shared__ double red[SOLVE_THREADS / 32 + 1];
+  __shared__ int flag;
+  const int n = S.d, C = S.C, L = S.count;
+  const int nn = n * n;
+  int* iscr = reinterpret_cast<int*>(sm);  // 2n+2 ints
+  double* base = sm + (2 * n + 2 + 1) / 2 + 1;
+  double *ja, *jtmp;
+  double* g = S.ws;
+  if (S.jacobi_in_smem) {
+    ja = base;
+    jtmp = base + nn;
+  } else {
+    ja = g;
+    jtmp = g + nn;
+    g += 2 * nn;
+  }
+  Blk B{red, &flag, iscr};
+  double* c11 = S.fin;
+  double* c22 = S.fin + nn;
+  double* ct = S.fin + 4 * nn;
+  double* R1 = g; g += nn;
+  double* R2 = g; g += nn;
+  double* T = g; g += nn;
+  double* Gm = g; g += nn;
+  double* U = g; g += nn;
+  double* V = g; g += nn;   // right vectors (n x L used)
+  double* NB = g; g += nn;  // null basis
+  double* ev = g; g += nn;  // eigvec scratch
+  double* lam = g; g += n;
+  double* wsc = g; g += 2 * n + 2;
+  double* sig = g; g += n;
+  double* flip = g; g += n;
+  double* lam2 = g; g += n;
+  if (threadIdx.x == 0) { flag = 0; *S.status = 0; }
+  __syncthreads();
+  // ---- finalize (moments.py:168-193); payload == nullptr: fin already holds finalized moments
+  if (S.payload != nullptr && !finalize_dev(S.payload, n, C, S.eps, S.fin, B)) {
+    if (threadIdx.x == 0) *S.status = DDCCA_ENUMERICAL;
+    return;
+  }
+  // ---- whitening (solver.py:227-229)
+  int rc = inv_sqrt_dev(c11, n, R1, lam, ev, ja, jtmp, wsc, B);
+  if (rc == DDCCA_OK) rc = inv_sqrt_dev(c22, n, R2, lam, ev, ja, jtmp, wsc, B);
+  if (rc != DDCCA_OK) {
+    if (threadIdx.x == 0) *S.status = rc;
+    return;
+  }
+  matmul(R1, false, ct, false, Gm, n, n, n);  // Gm = R1 ct
+  matmul(Gm, false, R2, false, T, n, n, n);   // T = R1 ct R2
+  matmul(T, false, T, true, Gm, n, n, n);     // Gm = T T^T
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    if (i <= j) {
+      const double x = 0.5 * (Gm[e] + Gm[j * n + i]);
+      ev[e] = x;
+      ev[j * n + i] = x;
+    }
+  }
+  __syncthreads();
+  rc = sym_eig_dev(ev, n, lam, U, ja, jtmp, wsc, B);
+  if (rc != DDCCA_OK) {
+    if (threadIdx.x == 0) *S.status = rc;
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sig[i] = sqrt(fmax(lam[i], 0.0));
+  __syncthreads();
+  // ---- right vectors, null-space completion (solver.py:235-247)
+  __shared__ int need_null;
+  if (threadIdx.x == 0) {
+    need_null = 0;
+    const double thr = 1e-12 * fmax(sig[0], 1e-300);
+    for (int k = 0; k < L; ++k)
+      if (!(sig[k] > thr)) need_null = 1;
+  }
+  __syncthreads();
+  if (need_null) {
+    matmul(T, true, T, false, Gm, n, n, n);  // T^T T
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      if (i <= j) {
+        const double x = 0.5 * (Gm[e] + Gm[j * n + i]);
+        ev[e] = x;
+        ev[j * n + i] = x;
+      }
+    }
+    __syncthreads();
+    rc = sym_eig_dev(ev, n, lam2, NB, ja, jtmp, wsc, B);
+    if (rc != DDCCA_OK) {
+      if (threadIdx.x == 0) *S.status = rc;
+      return;
+    }
+  }
+  // column k of V (n x L row-major)
+  __shared__ int null_src[64];
+  if (threadIdx.x == 0) {
+    const double thr = 1e-12 * fmax(sig[0], 1e-300);
+    int nxt = n - 1;
+    for (int k = 0; k < L; ++k) {
+      if (sig[k] > thr) {
+        null_src[k] = -1;
+      } else {
+        sig[k] = 0.0;
+        null_src[k] = nxt--;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * L; e += blockDim.x) {
+    const int i = e / L, k = e - i * L;
+    double val;
+    if (null_src[k] < 0) {
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) s += T[j * n + i] * U[j * n + k];
+      val = s / sig[k];
+    } else {
+      val = NB[i * n + null_src[k]];
+    }
+    V[e] = val;
+  }
+  __syncthreads();
+  // W1 = R1 U[:, :L], W2 = R2 V
+  for (int e = threadIdx.x; e < n * L; e += blockDim.x) {
+    const int i = e / L, k = e - i * L;
+    double s1 = 0.0, s2 = 0.0;
+    for (int j = 0; j < n; ++j) {
+      s1 += R1[i * n + j] * U[j * n + k];
+      s2 += R2[i * n + j] * V[j * L + k];
+    }
+    S.w1[e] = s1;
+    S.w2[e] = s2;
+  }
+  __syncthreads();
+  col_signs(S.w1, n, L, L, flip);
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * L; e += blockDim.x) {
+    const int k = e % L;
+    S.w1[e] *= flip[k];
+    S.w2[e] *= flip[k];
+  }
+  __syncthreads();
+  // zero-correlation columns of W2 re-signed independently (solver.py:254-256)
+  col_signs(S.w2, n, L, L, flip);
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * L; e += blockDim.x) {
+    const int k = e % L;
+    if (sig[k] == 0.0) S.w2[e] *= flip[k];
+  }
+  for (int k = threadIdx.x; k < L; k += blockDim.x) S.rho[k] = sig[k];
+  __syncthreads();
+  // conv-ready float32 packs: [tap][filter] == W row-major (reshape_filters, solver.py:260-272)
+  for (int e = threadIdx.x; e < n * L; e += blockDim.x) {
+    if (S.pack1) S.pack1[e] = (float)S.w1[e];
+    if (S.pack2) S.pack2[e] = (float)S.w2[e];
+  }
+}
+
+struct EigArgs {
+  const double* s;
+  int n, mode;
+  double *w, *v;
+  int32_t* status;
+  double* ws;
+  int jacobi_in_smem;
+};
+
+__global__ void __launch_bounds__(SOLVE_THREADS) sym_eig_kernel(EigArgs E) {
+  extern __shared__ double sm[];
+  __shared__ double red[SOLVE_THREADS / 32 + 1];
+  __shared__ int flag;
+  const int n = E.n, nn = n * n;
+  int* iscr = reinterpret_cast<int*>(sm);
+  double* base = sm + (2 * n + 2 + 1) / 2 + 1;
+  double* g = E.ws;
+  double *ja, *jtmp;
+  if (E.jacobi_in_smem) {
+    ja = base;
+    jtmp = base + nn;
+  } else {
+    ja = g;
+    jtmp = g + nn;
+    g += 2 * nn;
+  }
+  double* vv = g; g += nn;
+  double* wsc = g; g += 2 * n + 2;
+  Blk B{red, &flag, iscr};
+  int rc;
+  if (E.mode == 0) {
+    rc = sym_eig_dev(E.s, n, E.w, E.v, ja, jtmp, wsc, B);
+  } else {
+    rc = inv_sqrt_dev(E.s, n, E.v, E.w, vv, ja, jtmp, wsc, B);
+  }
+  if (threadIdx.x == 0) *E.status = rc;
+}
+
+__global__ void pack_kernel(const double* f, int n, float* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) out[e] = (float)f[e];
+}
+
+static size_t jacobi_smem(int n, bool in_smem) {
+  size_t ints = sizeof(double) * ((2 * n + 2 + 1) / 2 + 1);
+  return ints + (in_smem ? sizeof(double) * 2 * (size_t)n * n : 0);
+}
+
+}  // namespace ddcca
+
+using namespace ddcca;
+
+extern "C" {
+
+size_t ddcca_solve_workspace(int dim) {
+  const size_t nn = (size_t)dim * dim;
+  return sizeof(double) * (12 * nn + 8 * (size_t)dim + 16);
+}
+
+int ddcca_solve(const double* payload, int dim, int class_count, double epsilon, int count, double* fin, double* w1,
+                double* w2, double* rho, float* conv_pack1, float* conv_pack2, int32_t* status, void* ws,
+                size_t ws_bytes, void* stream) {
+  if (dim < 1 || class_count < 1) return fail(DDCCA_ECONFIG, "invalid accumulator shape dim=%d classes=%d", dim, class_count);
+  if (count < 1 || count > dim) return fail(DDCCA_ECONFIG, "filter count %d outside [1, %d]", count, dim);
+  if (count > 64) return fail(DDCCA_ECONFIG, "filter count %d above the device limit 64", count);
+  if (epsilon < 0) return fail(DDCCA_ECONFIG, "ridge coefficient %g must be >= 0", epsilon);
+  if (ws_bytes < ddcca_solve_workspace(dim)) return fail(DDCCA_ECONFIG, "solve workspace too small");
+  if (!fin || !w1 || !w2 || !rho || !status || !ws) return fail(DDCCA_ESHAPE, "null pointer");
+  const bool in_smem = dim <= SMEM_JACOBI_MAX_N;
+  const size_t sm = jacobi_smem(dim, in_smem);
+  SolveArgs S{payload, dim, class_count, count, epsilon, fin, w1, w2, rho, conv_pack1, conv_pack2, status,
+              static_cast<double*>(ws), in_smem ? 1 : 0};
+  cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  solve_kernel<<<1, SOLVE_THREADS, sm, as_stream(stream)>>>(S);
+  return check_launch("solve_kernel");
+}
+
+int ddcca_finalize(const double* payload, int dim, int class_count, double epsilon, double* fin, int32_t* status,
+                   void* stream) {
+  if (dim < 1 || class_count < 1) return fail(DDCCA_ECONFIG, "invalid accumulator shape dim=%d classes=%d", dim, class_count);
+  if (epsilon < 0) return fail(DDCCA_ECONFIG, "ridge coefficient %g must be >= 0", epsilon);
+  finalize_kernel<<<1, SOLVE_THREADS, 0, as_stream(stream)>>>(payload, dim, class_count, epsilon, fin, status);
+  return check_launch("finalize_kernel");
+}
+
+int ddcca_sym_eig(const double* s, int n, int mode, double* w, double* v, int32_t* status, void* ws, size_t ws_bytes,
+                  void* stream) {
+  if (n < 1) return fail(DDCCA_ESHAPE, "expected a square matrix");
+  if (ws_bytes < ddcca_solve_workspace(n)) return fail(DDCCA_ECONFIG, "eig workspace too small");
+  const bool in_smem = n <= SMEM_JACOBI_MAX_N;
+  const size_t sm = jacobi_smem(n, in_smem);
+  EigArgs E{s, n, mode, w, v, status, static_cast<double*>(ws), in_smem ? 1 : 0};
+  cudaFuncSetAttribute(sym_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  sym_eig_kernel<<<1, SOLVE_THREADS, sm, as_stream(stream)>>>(E);
+  return check_launch("sym_eig_kernel");
+}
+
+int ddcca_pack_filters(const double* filters, int count, int dim, float* conv_pack, void* stream) {
+  if (count < 1 || dim < 1) return fail(DDCCA_ECONFIG, "invalid filter bank %d x %d", count, dim);
+  pack_kernel<<<(count * dim + 255) / 256, 256, 0, as_stream(stream)>>>(filters, count * dim, conv_pack);
+  return check_launch("pack_filters");
+}
+
+}  // extern "C"

@@ -1,0 +1,436 @@
+"""Device-resident DDCCANet fit/transform engine (the hot path).
+
+Everything between the host inputs and the outputs runs as sm_100a kernels
+from libddcca (csrc/*.cu) on the executor's stream; torch supplies device
+memory, streams and torch.distributed (NCCL) for the one exchange per layer.
+
+Fit (cascade.train_network, cascade.py:207-223) per layer i:
+  for each super-batch of whole sample batches on this rank:
+    maps_i = forward through layers < i            (ddcca_conv, recomputed)
+    partials[b] = moments of batch b               (ddcca_moments_partial)
+  merged = fixed tree over all batches             (ddcca_moments_tree; NCCL
+                                                    all_gather or all_reduce)
+  layer_i = finalize + solve                       (ddcca_solve, 1 CTA FP64)
+Transform (pipeline.compute_features, pipeline.py:61-86):
+  for each super-batch: maps = forward through layers < S; last layer conv
+  fused with sign-hash (ddcca_conv_hash) -> block histograms
+  (ddcca_block_hist) written straight into the (M, featlen) count matrix;
+  optional LUT expansion to the reference's float64 features
+  (ddcca_iq_expand).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import ConfigError, ShapeError
+from .patches import PatchGeometry
+
+MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class DeviceLayer:
+    """A trained layer kept on the device (float64 vectors + float32 conv packs)."""
+
+    geom: PatchGeometry
+    center: bool
+    count: int
+    w1: object  # torch float64 (d, count)
+    w2: object
+    rho: object  # torch float64 (count,)
+    pack1: object  # torch float32 (d * count) tap-major
+    pack2: object
+    fin: object = None  # torch float64 (5, d, d): c11, c22, cw, cb, ctilde
+
+    def pack(self, view: int):
+        return self.pack1 if view == 1 else self.pack2
+
+
+# ----------------------------------------------------------------------------
+# thin op wrappers (one C-ABI call each)
+# ----------------------------------------------------------------------------
+
+def payload_len(dim: int, classes: int) -> int:
+    return int(_native.load().ddcca_payload_len(dim, classes))
+
+
+def moments_partials(ex, maps1, maps2, map_labels, batch_offsets: np.ndarray, geom: PatchGeometry, center: bool,
+                     classes: int, out=None):
+    """Per-batch partial accumulators (n_batches, payload_len) float64 on device."""
+    torch = _torch()
+    lib = _native.load()
+    n, p, q = maps1.shape
+    if maps2.shape != maps1.shape:
+        raise ShapeError(f"view map stacks differ: {tuple(maps1.shape)} vs {tuple(maps2.shape)}")
+    offs = np.ascontiguousarray(batch_offsets, dtype=np.int64)
+    nb = len(offs) - 1
+    g = geom.native(p, q)
+    max_maps = int(np.max(np.diff(offs)))
+    ws_bytes = int(lib.ddcca_moments_workspace(C.byref(g), nb, max_maps, classes))
+    plen = payload_len(geom.dim, classes)
+    if out is None:
+        out = torch.empty((nb, plen), dtype=torch.float64, device=ex.device)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=ex.device)
+    rc = lib.ddcca_moments_partial(_native.ptr(maps1), _native.ptr(maps2), _native.ptr(map_labels),
+                                   offs.ctypes.data_as(C.POINTER(C.c_int64)), nb, C.byref(g), int(bool(center)),
+                                   classes, _native.ptr(out), _native.ptr(ws), ws_bytes,
+                                   _native.stream_ptr(ex.stream))
+    _native.check(rc, "moments")
+    return out
+
+
+def tree_merge(ex, parts):
+    """Left-to-right pairwise tree over the rows of ``parts`` (moments.py:132-144); clobbers ``parts``."""
+    torch = _torch()
+    lib = _native.load()
+    n, plen = parts.shape
+    out = torch.empty(plen, dtype=torch.float64, device=ex.device)
+    _native.check(lib.ddcca_moments_tree(_native.ptr(parts), n, plen, _native.ptr(out),
+                                         _native.stream_ptr(ex.stream)), "pairwise_merge")
+    return out
+
+
+def solve_layer(ex, payload, geom: PatchGeometry, count: int, center: bool, classes: int, eps: float,
+                check: bool = True) -> DeviceLayer:
+    torch = _torch()
+    lib = _native.load()
+    d = geom.dim
+    dev = ex.device
+    fin = torch.empty((5, d, d), dtype=torch.float64, device=dev)
+    w1 = torch.empty((d, count), dtype=torch.float64, device=dev)
+    w2 = torch.empty((d, count), dtype=torch.float64, device=dev)
+    rho = torch.empty(count, dtype=torch.float64, device=dev)
+    pack1 = torch.empty(d * count, dtype=torch.float32, device=dev)
+    pack2 = torch.empty(d * count, dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws_bytes = int(lib.ddcca_solve_workspace(d))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    rc = lib.ddcca_solve(_native.ptr(payload), d, classes, float(eps), count, _native.ptr(fin), _native.ptr(w1),
+                         _native.ptr(w2), _native.ptr(rho), _native.ptr(pack1), _native.ptr(pack2),
+                         _native.ptr(status), _native.ptr(ws), ws_bytes, _native.stream_ptr(ex.stream))
+    _native.check(rc, "solve_dcca")
+    layer = DeviceLayer(geom, bool(center), count, w1, w2, rho, pack1, pack2, fin)
+    layer._status = status
+    if check:
+        check_layer(layer)
+    return layer
+
+
+def check_layer(layer: DeviceLayer) -> None:
+    st = getattr(layer, "_status", None)
+    if st is not None:
+        _native.status_error(int(st.item()), "solve_dcca")
+
+
+def layer_from_filters(ex, filters1, filters2, geom: PatchGeometry, center: bool) -> DeviceLayer:
+    """Upload host filter banks (L, l1, l2) as a DeviceLayer (for injected / loaded banks)."""
+    torch = _torch()
+    f1 = np.asarray(filters1, dtype=np.float64)
+    f2 = np.asarray(filters2, dtype=np.float64)
+    count = f1.shape[0]
+    if f1.shape != f2.shape or f1.shape[1:] != (geom.l1, geom.l2):
+        raise ShapeError(f"filter banks {f1.shape} / {f2.shape} do not match {geom.l1}x{geom.l2}")
+    w1 = torch.from_numpy(np.ascontiguousarray(f1.reshape(count, -1).T)).to(ex.device)
+    w2 = torch.from_numpy(np.ascontiguousarray(f2.reshape(count, -1).T)).to(ex.device)
+    lib = _native.load()
+    packs = []
+    for w in (w1, w2):
+        pk = torch.empty(geom.dim * count, dtype=torch.float32, device=ex.device)
+        _native.check(lib.ddcca_pack_filters(_native.ptr(w), count, geom.dim, _native.ptr(pk),
+                                             _native.stream_ptr(ex.stream)), "pack_filters")
+        packs.append(pk)
+    return DeviceLayer(geom, bool(center), count, w1, w2, None, packs[0], packs[1])
+
+
+def conv(ex, maps, layer: DeviceLayer, view: int, out=None):
+    """(n, p, q) float32 -> (n, L, oh, ow) float32 filter-minor (apply_filters, cascade.py:108-126)."""
+    torch = _torch()
+    lib = _native.load()
+    n, p, q = maps.shape
+    oh, ow = layer.geom.out_shape(p, q)
+    if out is None:
+        out = torch.empty((n, layer.count, oh, ow), dtype=torch.float32, device=ex.device)
+    g = layer.geom.native(p, q)
+    _native.check(lib.ddcca_conv(_native.ptr(maps), n, C.byref(g), _native.ptr(layer.pack(view)), layer.count,
+                                 int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream)), "conv")
+    return out
+
+
+def conv_hash(ex, maps, layer: DeviceLayer, view: int, out=None):
+    """Last-layer conv fused with sign-hash: (n, p, q) -> codes (n, oh, ow) u8/u16."""
+    torch = _torch()
+    lib = _native.load()
+    n, p, q = maps.shape
+    oh, ow = layer.geom.out_shape(p, q)
+    dt = torch.uint8 if layer.count <= 8 else torch.int16
+    if out is None:
+        out = torch.empty((n, oh, ow), dtype=dt, device=ex.device)
+    g = layer.geom.native(p, q)
+    _native.check(lib.ddcca_conv_hash(_native.ptr(maps), n, C.byref(g), _native.ptr(layer.pack(view)), layer.count,
+                                      int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream)),
+                  "conv_hash")
+    return out
+
+
+def count_kind(bpc: int) -> int:
+    """0: u8, 1: saturating u8 (decoded with the block sum), 2: u16."""
+    if bpc <= 255:
+        return 0
+    if bpc <= 510:
+        return 1
+    return 2
+
+
+def forward_maps(ex, images, layers: list, view: int):
+    """forward_stacks for one view (cascade.py:226-235): (b, p, q) -> (b * n_maps, p', q')."""
+    cur = images
+    for layer in layers:
+        n, p, q = cur.shape
+        out = conv(ex, cur, layer, view)
+        cur = out.view(n * layer.count, out.shape[2], out.shape[3])
+    return cur
+
+
+# ----------------------------------------------------------------------------
+# encoder geometry
+# ----------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class BlockPlan:
+    bh: int
+    bw: int
+    sh: int
+    sw: int
+    nby: int
+    nbx: int
+    n_bits: int
+
+    @property
+    def blocks(self) -> int:
+        return self.nby * self.nbx
+
+    @property
+    def bins(self) -> int:
+        return 1 << self.n_bits
+
+    @property
+    def bpc(self) -> int:
+        return self.bh * self.bw
+
+
+def block_plan(enc, p: int, q: int, n_bits: int) -> BlockPlan:
+    """EncoderConfig.block_starts (encoder.py:38-44) as a regular grid; Python round() = banker's."""
+    sh = max(1, int(round((1.0 - enc.overlap) * enc.block_h)))
+    sw = max(1, int(round((1.0 - enc.overlap) * enc.block_w)))
+    if p < enc.block_h or q < enc.block_w:
+        raise ShapeError(f"{enc.block_h}x{enc.block_w} blocks do not fit a {p}x{q} map")
+    nby = len(range(0, p - enc.block_h + 1, sh))
+    nbx = len(range(0, q - enc.block_w + 1, sw))
+    return BlockPlan(enc.block_h, enc.block_w, sh, sw, nby, nbx, n_bits)
+
+
+def iq_lut(enc) -> np.ndarray:
+    """Feature value for each count 0..bpc, bitwise equal to encoder.py:87-97 (same numpy log)."""
+    bpc = enc.block_h * enc.block_w
+    lut = np.empty(bpc + 1)
+    lut[0] = 0.0 if enc.zero_bin_policy == "zero" else float(np.log(2.0 * bpc))
+    lut[1:] = -np.log(np.arange(1, bpc + 1) / bpc)
+    return lut
+
+
+# ----------------------------------------------------------------------------
+# Engine
+# ----------------------------------------------------------------------------
+
+@dataclass
+class FitResult:
+    layers: list
+    stats: list = field(default_factory=list)  # per layer: merged payload (device)
+
+
+class Engine:
+    """Fit + transform on device for one executor (one GPU, one sample shard)."""
+
+    def __init__(self, executor, map_budget_bytes: int = MAP_BUDGET_BYTES):
+        self.ex = executor
+        self.budget = map_budget_bytes
+
+    # -- helpers -------------------------------------------------------------
+    def _superbatches(self, batch_ranges: list, bytes_per_sample: int):
+        """Group consecutive sample batches so one group's deepest maps fit the budget."""
+        groups, cur, cur_n = [], [], 0
+        for r in batch_ranges:
+            n = len(r)
+            if cur and (cur_n + n) * bytes_per_sample > self.budget:
+                groups.append(cur)
+                cur, cur_n = [], 0
+            cur.append(r)
+            cur_n += n
+        if cur:
+            groups.append(cur)
+        return groups
+
+    @staticmethod
+    def _maps_per_sample(layers: list) -> int:
+        return int(np.prod([lay.count for lay in layers])) if layers else 1
+
+    def _shape_after(self, p: int, q: int, layers: list):
+        for lay in layers:
+            p, q = lay.geom.out_shape(p, q)
+        return p, q
+
+    # -- fit -------------------------------------------------------------------
+    def layer_partials(self, images1, images2, labels, layers: list, geom: PatchGeometry, center: bool,
+                       classes: int, batch_ranges: list, first_sample: int = 0):
+        """Per-batch partial moments for the given (local) batches; returns (n_batches, plen)."""
+        torch = _torch()
+        ex = self.ex
+        _, p0, q0 = images1.shape
+        p, q = self._shape_after(p0, q0, layers)
+        n_in = self._maps_per_sample(layers)
+        plen = payload_len(geom.dim, classes)
+        parts = torch.empty((len(batch_ranges), plen), dtype=torch.float64, device=ex.device)
+        row = 0
+        for group in self._superbatches(batch_ranges, n_in * p * q * 4):
+            s0, s1 = group[0].start - first_sample, group[-1].stop - first_sample
+            m1 = forward_maps(ex, images1[s0:s1], layers, 1)
+            m2 = forward_maps(ex, images2[s0:s1], layers, 2)
+            mlab = labels[s0:s1].repeat_interleave(n_in) if n_in > 1 else labels[s0:s1]
+            offs = np.cumsum([0] + [len(r) * n_in for r in group], dtype=np.int64)
+            moments_partials(ex, m1, m2, mlab, offs, geom, center, classes, out=parts[row:row + len(group)])
+            row += len(group)
+        return parts
+
+    def reduce_partials(self, parts, n_global_batches: int, local_batches: range):
+        """Merged accumulator over all ranks' batches (fixed tree or sum-allreduce)."""
+        torch = _torch()
+        ex = self.ex
+        if ex.world_size == 1:
+            return tree_merge(ex, parts)
+        dist = torch.distributed
+        if ex.deterministic:
+            # gather every rank's per-batch partials, rebuild global batch order, same tree everywhere
+            from .execution import shard_range
+
+            counts = [len(shard_range(n_global_batches, r, ex.world_size)) for r in range(ex.world_size)]
+            mx = max(counts)
+            pad = torch.zeros((mx, parts.shape[1]), dtype=parts.dtype, device=ex.device)
+            pad[: parts.shape[0]] = parts
+            bufs = [torch.empty_like(pad) for _ in range(ex.world_size)]
+            with torch.cuda.stream(ex.stream):
+                dist.all_gather(bufs, pad, group=ex.group)
+            allp = torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0).contiguous()
+            return tree_merge(ex, allp)
+        merged = tree_merge(ex, parts)
+        with torch.cuda.stream(ex.stream):
+            dist.all_reduce(merged, group=ex.group)
+        return merged
+
+    def fit(self, images1, images2, labels, classes: int, layer_cfgs: list, batch_size: int, eps: float,
+            n_global: int | None = None, first_sample: int = 0, keep_stats: bool = False,
+            stage_hook=None) -> FitResult:
+        """Train all layers. images*: (m_local, p, q) float32 device; labels: (m_local,) int32 device.
+
+        ``n_global`` / ``first_sample`` describe the global sample set when this
+        rank holds only its shard (samples [first_sample, first_sample + m_local)).
+        """
+        torch = _torch()
+        ex = self.ex
+        m_local = images1.shape[0]
+        n_global = m_local if n_global is None else n_global
+        gb = [range(s, min(s + batch_size, n_global)) for s in range(0, n_global, batch_size)]
+        mine = ex.shard(len(gb))
+        local = [gb[b] for b in mine]
+        if local and (local[0].start != first_sample or local[-1].stop - first_sample != m_local):
+            raise ShapeError("local images do not match this rank's batch shard")
+        layers, stats = [], []
+        with torch.cuda.stream(ex.stream):
+            for i, cfg in enumerate(layer_cfgs):
+                if stage_hook:
+                    stage_hook(f"layer {i + 1}: accumulating moments over {len(gb)} batches")
+                parts = self.layer_partials(images1, images2, labels, layers, cfg.geom, cfg.center, classes, local,
+                                            first_sample)
+                merged = self.reduce_partials(parts, len(gb), mine)
+                layer = solve_layer(ex, merged, cfg.geom, cfg.filters, cfg.center, classes, eps)
+                layers.append(layer)
+                if keep_stats:
+                    stats.append(merged)
+        return FitResult(layers, stats)
+
+    # -- transform ---------------------------------------------------------
+    def feature_geometry(self, p0: int, q0: int, layers: list, enc):
+        p, q = self._shape_after(p0, q0, layers)
+        n_bits = layers[-1].count
+        if not 1 <= n_bits <= 16:
+            raise ConfigError(f"device hashing supports 1..16 bit maps, got {n_bits}")
+        plan = block_plan(enc, p, q, n_bits)
+        groups = self._maps_per_sample(layers[:-1])
+        featlen = 2 * groups * plan.blocks * plan.bins
+        return plan, groups, featlen
+
+    def transform_counts(self, images1, images2, layers: list, enc, batch_size: int, out=None):
+        """(m, p, q) x2 -> per-sample block counts (m, featlen) u8/u16 on device."""
+        torch = _torch()
+        ex = self.ex
+        lib = _native.load()
+        m, p0, q0 = images1.shape
+        plan, groups, featlen = self.feature_geometry(p0, q0, layers, enc)
+        kind = count_kind(plan.bpc)
+        dt = torch.int16 if kind == 2 else torch.uint8
+        if out is None:
+            out = torch.empty((m, featlen), dtype=dt, device=ex.device)
+        ranges = [range(s, min(s + batch_size, m)) for s in range(0, m, batch_size)]
+        pm, qm = self._shape_after(p0, q0, layers[:-1])
+        per_view = groups * plan.blocks * plan.bins
+        with torch.cuda.stream(ex.stream):
+            for group in self._superbatches(ranges, groups * pm * qm * 4):
+                s0, s1 = group[0].start, group[-1].stop
+                for view, imgs in ((1, images1), (2, images2)):
+                    maps = forward_maps(ex, imgs[s0:s1], layers[:-1], view)
+                    codes = conv_hash(ex, maps, layers[-1], view)
+                    base = out[s0:s1].view(-1)[(view - 1) * per_view:]
+                    _native.check(lib.ddcca_block_hist(
+                        _native.ptr(codes), codes.element_size(), codes.shape[0], codes.shape[1], codes.shape[2],
+                        plan.n_bits, plan.bh, plan.bw, plan.sh, plan.sw, _native.ptr(base), kind, groups, featlen,
+                        plan.blocks * plan.bins, _native.stream_ptr(ex.stream)), "block_hist")
+        return out, plan
+
+    def expand(self, counts, plan: BlockPlan, enc):
+        """Counts -> float64 IQ features (iq_block_features values) on device."""
+        torch = _torch()
+        ex = self.ex
+        lib = _native.load()
+        lut = torch.from_numpy(iq_lut(enc)).to(ex.device)
+        out = torch.empty(counts.shape, dtype=torch.float64, device=ex.device)
+        nblk = counts.numel() // plan.bins
+        _native.check(lib.ddcca_iq_expand(_native.ptr(counts), count_kind(plan.bpc), nblk, plan.n_bits, plan.bpc,
+                                          _native.ptr(lut), _native.ptr(out), _native.stream_ptr(ex.stream)),
+                      "iq_expand")
+        return out
+
+
+def decode_counts(counts: np.ndarray, plan: BlockPlan) -> np.ndarray:
+    """Host-side view of device counts as exact integers (undo the saturating u8 form)."""
+    c = np.asarray(counts)
+    if c.dtype == np.int16:
+        return c.view(np.uint16).astype(np.int64)
+    c = c.astype(np.int64)
+    if count_kind(plan.bpc) == 1:
+        blk = c.reshape(-1, plan.bins)
+        extra = plan.bpc - blk.sum(axis=1)
+        sat = blk == 255
+        blk[sat] += np.repeat(extra, sat.sum(axis=1))
+        c = blk.reshape(c.shape)
+    return c

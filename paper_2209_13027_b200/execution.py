@@ -1,0 +1,104 @@
+"""Execution settings and the device executor.
+
+Reference: execution.py:15-68 defines ``ExecSettings(threads, deterministic,
+seed)`` and a thread-pool ``Executor`` whose ``map_ordered`` fans sample
+batches out to CPU threads. On B200 the unit of parallelism is one process
+per GPU: the executor binds this process to one CUDA device and one stream,
+knows its rank in the (optional) ``torch.distributed`` process group, owns
+the sample-batch sharding, and performs the one exchange the path needs —
+the per-layer reduction of partial moments (NCCL over NVLink). The host
+``map_ordered`` / ``map_completion_order`` helpers are kept for callers that
+use the executor as a generic map (they run inline, in order).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+from .errors import ConfigError
+
+
+@dataclass(frozen=True)
+class ExecSettings:
+    """Same fields as the reference (execution.py:15-23).
+
+    ``threads`` is accepted for API compatibility; on the device path the
+    parallelism is the GPU grid and the number of ranks. ``deterministic``
+    selects the reduction: True -> per-batch partials gathered from all ranks
+    and merged through the reference's fixed left-to-right tree (bitwise
+    independent of the GPU count); False -> local tree + one sum-allreduce.
+    """
+
+    threads: int = 1
+    deterministic: bool = True
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.threads < 1:
+            raise ConfigError(f"thread count {self.threads} must be >= 1")
+
+
+class Executor:
+    """One CUDA device + stream, plus the process group of the sample shards."""
+
+    def __init__(self, settings: ExecSettings | None = None, device=None, process_group=None, stream=None):
+        import torch
+
+        self.settings = settings or ExecSettings()
+        if not torch.cuda.is_available():
+            from ._native import DeviceError
+
+            raise DeviceError("no CUDA device visible: the ddcca path runs only on the GPU (no CPU fallback)")
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device()))
+        self.device = torch.device("cuda", device) if not isinstance(device, torch.device) else device
+        torch.cuda.set_device(self.device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.group = process_group
+        dist = torch.distributed
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(process_group)
+            self.world_size = dist.get_world_size(process_group)
+        else:
+            self.rank, self.world_size = 0, 1
+
+    # -- reference surface ------------------------------------------------
+    @property
+    def threads(self) -> int:
+        return self.settings.threads
+
+    @property
+    def deterministic(self) -> bool:
+        return self.settings.deterministic
+
+    def map_ordered(self, fn, items) -> list:
+        return [fn(item) for item in items]
+
+    def map_completion_order(self, fn, items):
+        for item in items:
+            yield fn(item)
+
+    def close(self):
+        self.synchronize()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- device side --------------------------------------------------------
+    def synchronize(self):
+        self.stream.synchronize()
+
+    def shard(self, n_batches: int) -> range:
+        """Contiguous range of global batch indices owned by this rank."""
+        return shard_range(n_batches, self.rank, self.world_size)
+
+
+def shard_range(n_batches: int, rank: int, world: int) -> range:
+    """Balanced contiguous split of ``n_batches`` over ``world`` ranks (first ranks get the remainder)."""
+    base, extra = divmod(n_batches, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))

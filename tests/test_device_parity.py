@@ -1,0 +1,296 @@
+"""GPU parity: every device kernel against the CPU oracle and the reference's golden vectors.
+
+Tolerances (north_star): covariances rel. Frobenius <= 1e-5 (we reach ~1e-12:
+float64 products of float32 inputs are exact); filters |cos| >= 0.9999 on
+well-posed indices; features bit-exact except where the reference response
+lies within 1e-6 of the binarization threshold (>= 99.9 % bins identical).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2209_13027_b200 as P  # noqa: E402
+from paper_2209_13027_b200 import engine as E  # noqa: E402
+from paper_2209_13027_b200 import synthetic  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ex():
+    return P.Executor(P.ExecSettings())
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
+
+
+def oracle_acc(maps1, maps2, labels, geom, center, classes, batch):
+    return O.layer_stats(maps1.astype(np.float64), maps2.astype(np.float64), labels,
+                         O.Geometry(geom.l1, geom.l2, geom.stride, geom.padding), center, classes, batch, O.Pool())
+
+
+# ------------------------------------------------------------------------ moments
+
+GEOMS = [
+    (5, 5, 1, "zero_same"), (7, 7, 1, "zero_same"), (3, 3, 1, "zero_same"), (2, 4, 1, "zero_same"),
+    (4, 6, 1, "zero_same"), (1, 1, 1, "zero_same"), (3, 5, 1, "none"), (9, 9, 1, "zero_same"),
+    (5, 5, 2, "zero_same"), (3, 3, 3, "none"), (6, 2, 1, "zero_same"), (12, 12, 1, "zero_same"),
+]
+
+
+@pytest.mark.parametrize("l1,l2,stride,padding", GEOMS)
+@pytest.mark.parametrize("center", [True, False])
+def test_layer_moments_match_oracle(ex, l1, l2, stride, padding, center):
+    rng = np.random.default_rng(l1 * 100 + l2 * 10 + stride)
+    n, nm, p, q, classes = 11, 2, 19, 23, 3
+    m1 = rng.uniform(size=(n, nm, p, q)).astype(np.float32)
+    m2 = rng.standard_normal((n, nm, p, q)).astype(np.float32)
+    lab = rng.integers(0, classes, n)
+    geom = P.PatchGeometry(l1, l2, stride, padding)
+    out = P.LayerOutput(m1, m2, lab, tuple((i,) for i in range(nm)))
+    got = P.accumulate_layer_moments(out, geom, center, classes, P.BatchSpec(4), ex)
+    ref = oracle_acc(m1, m2, lab, geom, center, classes, 4)
+    for f, g in (("c11", "c11"), ("c22", "c22"), ("class_sum1", "s1"), ("class_sum2", "s2"),
+                 ("global_sum1", "g1"), ("global_sum2", "g2")):
+        assert rel(getattr(got, f), getattr(ref, g)) <= 1e-11, f
+    assert got.patch_count == ref.n
+    assert np.array_equal(got.per_class_patch_count, ref.n_class)
+
+
+def test_tiny_maps_smaller_than_window(ex):
+    # oh < l1 - 1: every padded row is its own zone
+    rng = np.random.default_rng(1)
+    m1 = rng.uniform(size=(5, 1, 3, 2)).astype(np.float32)
+    m2 = rng.uniform(size=(5, 1, 3, 2)).astype(np.float32)
+    lab = np.array([0, 1, 0, 1, 1])
+    geom = P.PatchGeometry(7, 5)
+    got = P.accumulate_layer_moments(P.LayerOutput(m1, m2, lab, ((),)), geom, True, 2, P.BatchSpec(2), ex)
+    ref = oracle_acc(m1, m2, lab, geom, True, 2, 2)
+    assert rel(got.c11, ref.c11) <= 1e-11 and rel(got.class_sum2, ref.s2) <= 1e-11
+
+
+def test_moments_golden_pipeline_layer1(ex, golden):
+    g = golden("pipeline_orl_mini")
+    L, l1, l2 = (int(v) for v in g["layers"][0])
+    ds = P.ViewPairDataset.from_arrays(g["v1"].astype(np.float32), g["v2"].astype(np.float32), g["labels"],
+                                       class_count=int(g["classes"]))
+    acc = P.accumulate_layer_moments(P.layer_input(ds), P.PatchGeometry(l1, l2), True, int(g["classes"]),
+                                     P.BatchSpec(int(g["batch"])), ex)
+    assert rel(acc.c11, g["acc1_c11"]) <= 1e-10
+    assert rel(acc.c22, g["acc1_c22"]) <= 1e-10
+    assert rel(acc.class_sum1, g["acc1_s1"]) <= 1e-10
+    assert rel(acc.global_sum2, g["acc1_g2"]) <= 1e-10
+    assert acc.patch_count == int(g["acc1_n"])
+
+
+def test_batch_tree_is_reference_tree(ex):
+    # per-batch partials merged on device == oracle's pairwise tree of per-batch accumulators
+    rng = np.random.default_rng(7)
+    parts = rng.standard_normal((13, 57))
+    got = E.tree_merge(ex, torch.from_numpy(parts.copy()).to(ex.device)).cpu().numpy()
+    level = [parts[i] for i in range(13)]
+    while len(level) > 1:
+        nxt = [level[i] + level[i + 1] for i in range(0, len(level) - 1, 2)]
+        if len(level) % 2:
+            nxt.append(level[-1])
+        level = nxt
+    assert np.array_equal(got, level[0])
+
+
+def test_accumulate_batch_columns(ex, golden):
+    g = golden("moments")
+    acc = P.MomentAccumulator.zeros(6, 3)
+    P.accumulate_batch(acc, g["x"][:, :17], g["y"][:, :17], g["labels"][:17], ex)
+    P.accumulate_batch(acc, g["x"][:, 17:], g["y"][:, 17:], g["labels"][17:], ex)
+    assert rel(acc.c11, g["c11"]) <= 1e-13 and rel(acc.class_sum2, g["s2"]) <= 1e-13
+    assert acc.patch_count == int(g["n"]) and np.array_equal(acc.per_class_patch_count, g["n_class"])
+    fin = P.finalize(acc, 1e-4, ex)
+    assert rel(fin.ctilde, g["f_ct"]) <= 1e-12 and rel(fin.c11, g["f_c11"]) <= 1e-13
+    with pytest.raises(P.ShapeError):
+        P.accumulate_batch(acc, np.zeros((3, 5)), np.zeros((3, 5)), np.zeros(5, int), ex)
+
+
+# ------------------------------------------------------------------------ solver
+
+def test_sym_eig_golden(ex, golden):
+    g = golden("solver")
+    k = 0
+    while f"c11_{k}" in g:
+        c = g[f"c11_{k}"]
+        w, v = P.sym_eig(0.5 * (c + c.T), ex)
+        assert np.allclose(w, g[f"eigw_{k}"], rtol=1e-12, atol=0)
+        assert rel(v, g[f"eigv_{k}"]) <= 1e-9
+        k += 1
+    w, v = P.sym_eig(np.diag([2.0, 5.0, 2.0, 2.0, 1.0]), ex)
+    assert np.array_equal(w, g["deg_w"]) and np.array_equal(v, g["deg_v"])
+
+
+def test_sym_eig_hard_spectra(ex):
+    # test_solver.py:88-104
+    rng = np.random.default_rng(21)
+    qm, _ = np.linalg.qr(rng.standard_normal((48, 48)))
+    hard = {
+        "huge condition": (qm * np.geomspace(1.0, 1e12, 48)) @ qm.T,
+        "clustered": (qm * np.repeat([1.0, 2.0, 3.0, 4.0], 12)) @ qm.T,
+        "rank one": np.outer(qm[:, 0], qm[:, 0]),
+        "extreme scale": 1e-300 * ((qm * np.arange(1.0, 49.0)) @ qm.T),
+        "negative definite": -((qm * np.geomspace(1.0, 100.0, 48)) @ qm.T),
+    }
+    for name, s in hard.items():
+        w, v = P.sym_eig(s, ex)
+        norm = np.linalg.norm(s)
+        assert np.linalg.norm(s @ v - v * w) <= 1e-8 * norm, name
+        assert np.abs(v.T @ v - np.eye(48)).max() <= 1e-10, name
+        ref = np.sort(np.linalg.eigvalsh(s))[::-1]
+        assert np.abs(w - ref).max() <= 1e-9 * max(np.abs(ref).max(), 1e-300), name
+
+
+def test_sym_eig_errors(ex):
+    with pytest.raises(P.ShapeError):
+        P.sym_eig(np.array([[1.0, 2.0], [0.0, 1.0]]), ex)
+    with pytest.raises(P.NumericalError):
+        P.inv_sqrt(np.diag([1.0, 0.0]), ex)
+    w, v = P.sym_eig(np.zeros((3, 3)), ex)
+    assert np.array_equal(w, np.zeros(3)) and np.array_equal(v, np.eye(3))
+    assert np.allclose(P.inv_sqrt(np.diag([4.0, 9.0]), ex), np.diag([0.5, 1.0 / 3.0]))
+
+
+def test_solve_dcca_golden(ex, golden):
+    g = golden("solver")
+    k = 0
+    while f"c11_{k}" in g:
+        ct = g[f"ct_{k}"]
+        m = P.DiscriminantMoments(g[f"c11_{k}"], g[f"c22_{k}"], ct, np.zeros_like(ct), ct, 1)
+        pr = P.solve_dcca(m, int(g[f"count_{k}"]), ex)
+        assert np.allclose(pr.rho, g[f"rho_{k}"], rtol=1e-9, atol=0), k
+        for j in range(pr.count):
+            for a, b in ((pr.w1[:, j], g[f"w1_{k}"][:, j]), (pr.w2[:, j], g[f"w2_{k}"][:, j])):
+                cos = a @ b / (np.linalg.norm(a) * np.linalg.norm(b))
+                assert cos >= 1 - 1e-9, (k, j, cos)
+        k += 1
+    m = P.DiscriminantMoments(g["zc_c"], g["zc_c"], np.zeros((4, 4)), np.zeros((4, 4)), np.zeros((4, 4)), 1)
+    pr = P.solve_dcca(m, 3, ex)
+    assert np.array_equal(pr.rho, g["zc_rho"])
+    assert rel(pr.w1, g["zc_w1"]) <= 1e-8 and rel(pr.w2, g["zc_w2"]) <= 1e-8
+
+
+# ------------------------------------------------------------------------ conv / encoder
+
+def test_conv_golden(ex, golden):
+    g = golden("conv")
+    k = 0
+    while f"filt{k}" in g:
+        f = g[f"filt{k}"]
+        for center in (0, 1):
+            lay = P.FilterLayer(f, f, P.PatchGeometry(f.shape[1], f.shape[2]), bool(center))
+            got = P.apply_filters(g["stack"], lay, 1, ex)
+            ref = g[f"out{k}_{center}"]
+            scale = np.abs(f).sum() * np.abs(g["stack"]).max()
+            assert np.abs(got - ref).max() <= 2e-6 * scale, (k, center)
+        k += 1
+    assert P.conv2d(np.array([[1.0, 2.0], [3.0, 4.0]]), np.ones((2, 2)), executor=ex).tolist() == [[10, 6], [7, 4]]
+
+
+@pytest.mark.parametrize("l1,l2,count,stride,padding", [(5, 5, 8, 1, "zero_same"), (7, 7, 8, 1, "zero_same"),
+                                                        (9, 9, 12, 1, "zero_same"), (3, 4, 5, 1, "none"),
+                                                        (6, 6, 16, 1, "zero_same"), (5, 5, 3, 2, "zero_same"),
+                                                        (7, 7, 40, 1, "zero_same")])
+def test_conv_random_vs_oracle(ex, l1, l2, count, stride, padding):
+    rng = np.random.default_rng(l1 * 7 + count)
+    stack = rng.uniform(size=(6, 37, 29)).astype(np.float32)
+    f = rng.standard_normal((count, l1, l2))
+    geom = P.PatchGeometry(l1, l2, stride, padding)
+    for center in (True, False):
+        got = P.apply_filters(stack, P.FilterLayer(f, f, geom, center), 2, ex)
+        ref = O.conv_stack(stack, O.Layer(f, f, O.Geometry(l1, l2, stride, padding), center), 2)
+        assert got.shape == ref.shape
+        scale = np.abs(f).sum(axis=(1, 2)).max()
+        assert np.abs(got - ref).max() <= 3e-6 * scale
+
+
+def test_encoder_golden(ex, golden):
+    g = golden("encoder")
+    k = 0
+    while f"cfg{k}" in g:
+        bh, bw, ov, pol, nb = g[f"cfg{k}"]
+        cfg = P.EncoderConfig(int(bh), int(bw), float(ov), "floor" if pol else "zero")
+        got = P.encode_view(g["maps"], int(nb), cfg, ex)
+        assert np.array_equal(got, g[f"feat{k}"]), k
+        k += 1
+
+
+def test_encoder_kats(ex):
+    assert P.binarize(np.array([[2.5, 0.0, -1.3]]), ex).tolist() == [[1, 0, 0]]
+    bits = np.zeros((8, 1, 1), dtype=int)
+    bits[0] = 1
+    bits[2] = 1
+    assert P.hash_combine(bits, ex)[0, 0] == 5
+    seg = P.iq_block_features(np.array([[0, 0], [3, 3]]), P.EncoderConfig(2, 2), 2, ex)
+    assert seg[0] == pytest.approx(np.log(2.0)) and seg[1] == seg[2] == 0.0
+
+
+@pytest.mark.parametrize("bh,bw,nb", [(16, 16, 8), (7, 7, 8), (20, 20, 6), (8, 8, 12)])
+def test_histogram_count_kinds_exact(ex, bh, bw, nb):
+    # u8 / saturating-u8 / u16 count storage all decode to the exact histogram
+    rng = np.random.default_rng(bh + nb)
+    maps = rng.standard_normal((2 * nb, 2 * bh + 3, 3 * bw + 1)).astype(np.float32)
+    maps[:nb, :bh, :bw] = 1.0  # a block with one code only (count == bpc)
+    cfg = P.EncoderConfig(bh, bw)
+    got = P.encode_view(maps, nb, cfg, ex)
+    assert np.array_equal(got, O.encode_maps(maps.astype(np.float64), nb, O.EncodeCfg(bh, bw)))
+
+
+# ------------------------------------------------------------------------ end to end
+
+def _oracle_layers(bank):
+    return [O.Layer(l.filters1, l.filters2, O.Geometry(l.geom.l1, l.geom.l2, l.geom.stride, l.geom.padding), l.center)
+            for l in bank.layers]
+
+
+@pytest.mark.parametrize("name", ["pipeline_small", "pipeline_orl_mini"])
+def test_transform_with_reference_filters(ex, golden, name):
+    g = golden(name)
+    geoms = [P.PatchGeometry(int(l1), int(l2)) for _, l1, l2 in g["layers"]]
+    bank = P.FilterBank(tuple(P.FilterLayer(g[f"f1_{i}"], g[f"f2_{i}"], geoms[i], True) for i in range(len(geoms))))
+    ds = P.ViewPairDataset.from_arrays(g["v1"].astype(np.float32), g["v2"].astype(np.float32), g["labels"])
+    bh, bw = (int(v) for v in g["block"])
+    net = P.NetworkConfig(tuple(P.LayerConfig(int(L), geoms[i]) for i, (L, _, _) in enumerate(g["layers"])),
+                          batch=P.BatchSpec(int(g["batch"])))
+    cfg = type("Cfg", (), {"net": net, "encoder": P.EncoderConfig(bh, bw)})()
+    got = P.compute_features(ds, bank, cfg, ex)
+    assert got.shape == g["features"].shape
+    assert np.mean(got == g["features"]) >= 0.999
+
+
+def test_fit_transform_end_to_end_vs_oracle(ex):
+    v1, lab = synthetic.blob_images(96, 28, 23, 6, seed=4)
+    v2 = synthetic.lbp_maps(v1)
+    ds = P.ViewPairDataset.from_arrays(v1, v2, lab, class_count=6)
+    geom = P.PatchGeometry(5, 5)
+    net = P.NetworkConfig((P.LayerConfig(4, geom), P.LayerConfig(4, geom)), batch=P.BatchSpec(32))
+    bank = P.train_network(ds, net, ex)
+    specs = [(4, O.Geometry(5, 5), True)] * 2
+    ref_layers, stats = O.train(v1.astype(np.float64), v2.astype(np.float64), lab, 6, specs, batch=32,
+                                return_stats=True)
+    # layer 1: same inputs -> filters agree on well-posed indices
+    rho = O.dcca_solve(stats[0][1], 4).rho
+    lam = rho ** 2
+    for j in range(4):
+        gaps = [abs(lam[j] - lam[k]) for k in range(4) if k != j]
+        if min(gaps) <= 1e-6 * lam[0] or rho[j] <= 1e-10 * rho[0]:
+            continue
+        for a, b in ((bank.layers[0].filters1[j], ref_layers[0].f1[j]), (bank.layers[0].filters2[j], ref_layers[0].f2[j])):
+            cos = abs((a * b).sum()) / (np.linalg.norm(a) * np.linalg.norm(b))
+            assert cos >= 0.9999, (j, cos)
+    # transform with the device's own bank matches the oracle transform of that bank
+    cfg = type("Cfg", (), {"net": net, "encoder": P.EncoderConfig(7, 7)})()
+    got = P.compute_features(ds, bank, cfg, ex)
+    want = O.features(v1, v2, _oracle_layers(bank), O.EncodeCfg(7, 7), batch=32)
+    assert np.mean(got == want) >= 0.999
