@@ -266,6 +266,36 @@ class Engine:
     def __init__(self, executor, map_budget_bytes: int = MAP_BUDGET_BYTES):
         self.ex = executor
         self.budget = map_budget_bytes
+        self.profile = None   # dict name -> [(start_event, end_event)] when profiling
+        self.work = {}        # name -> algorithmic work of one call (for the roofline)
+        self.launches = 0     # kernels launched by this engine
+
+    def _timed(self, name: str, kernels: int, work: dict | None, fn, *a, **k):
+        self.launches += kernels
+        if work is not None:
+            self.work[name] = work
+        if self.profile is None:
+            return fn(*a, **k)
+        torch = _torch()
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record(self.ex.stream)
+        out = fn(*a, **k)
+        e.record(self.ex.stream)
+        self.profile.setdefault(name, []).append((s, e))
+        return out
+
+    def _forward(self, images, layers: list, view: int):
+        cur = images
+        for li, layer in enumerate(layers):
+            n, p, q = cur.shape
+            oh, ow = layer.geom.out_shape(p, q)
+            fl = 2.0 * n * oh * ow * layer.count * layer.geom.dim
+            by = 4.0 * n * (p * q + layer.count * oh * ow)
+            out = self._timed(f"conv_l{li + 1}", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv, self.ex, cur,
+                              layer, view)
+            cur = out.view(n * layer.count, oh, ow)
+        return cur
 
     # -- helpers -------------------------------------------------------------
     def _superbatches(self, batch_ranges: list, bytes_per_sample: int):
@@ -305,11 +335,17 @@ class Engine:
         row = 0
         for group in self._superbatches(batch_ranges, n_in * p * q * 4):
             s0, s1 = group[0].start - first_sample, group[-1].stop - first_sample
-            m1 = forward_maps(ex, images1[s0:s1], layers, 1)
-            m2 = forward_maps(ex, images2[s0:s1], layers, 2)
+            m1 = self._forward(images1[s0:s1], layers, 1)
+            m2 = self._forward(images2[s0:s1], layers, 2)
             mlab = labels[s0:s1].repeat_interleave(n_in) if n_in > 1 else labels[s0:s1]
             offs = np.cumsum([0] + [len(r) * n_in for r in group], dtype=np.int64)
-            moments_partials(ex, m1, m2, mlab, offs, geom, center, classes, out=parts[row:row + len(group)])
+            nmaps = int(offs[-1])
+            top, bottom, left, right = geom.pad_amounts(p, q)
+            ndx = -(-(2 * geom.l2 - 1) // 3) * 3
+            fl = 2.0 * 2 * nmaps * (p + top + bottom) * (q + left + right) * geom.l1 * ndx
+            self._timed(f"moments_l{len(layers) + 1}", 5, {"kind": "fp64", "flops": fl, "bytes": 8.0 * nmaps * p * q},
+                        moments_partials, ex, m1, m2, mlab, offs, geom, center, classes,
+                        out=parts[row:row + len(group)])
             row += len(group)
         return parts
 
@@ -317,8 +353,9 @@ class Engine:
         """Merged accumulator over all ranks' batches (fixed tree or sum-allreduce)."""
         torch = _torch()
         ex = self.ex
+        levels = max(1, int(math.ceil(math.log2(max(parts.shape[0], 1))))) if parts.shape[0] > 1 else 0
         if ex.world_size == 1:
-            return tree_merge(ex, parts)
+            return self._timed("tree", levels, None, tree_merge, ex, parts)
         dist = torch.distributed
         if ex.deterministic:
             # gather every rank's per-batch partials, rebuild global batch order, same tree everywhere
@@ -363,7 +400,8 @@ class Engine:
                 parts = self.layer_partials(images1, images2, labels, layers, cfg.geom, cfg.center, classes, local,
                                             first_sample)
                 merged = self.reduce_partials(parts, len(gb), mine)
-                layer = solve_layer(ex, merged, cfg.geom, cfg.filters, cfg.center, classes, eps)
+                layer = self._timed(f"solve_l{i + 1}", 1, None, solve_layer, ex, merged, cfg.geom, cfg.filters,
+                                    cfg.center, classes, eps)
                 layers.append(layer)
                 if keep_stats:
                     stats.append(merged)
@@ -398,13 +436,22 @@ class Engine:
             for group in self._superbatches(ranges, groups * pm * qm * 4):
                 s0, s1 = group[0].start, group[-1].stop
                 for view, imgs in ((1, images1), (2, images2)):
-                    maps = forward_maps(ex, imgs[s0:s1], layers[:-1], view)
-                    codes = conv_hash(ex, maps, layers[-1], view)
+                    maps = self._forward(imgs[s0:s1], layers[:-1], view)
+                    last = layers[-1]
+                    n, pp, qq = maps.shape
+                    oh, ow = last.geom.out_shape(pp, qq)
+                    fl = 2.0 * n * oh * ow * last.count * last.geom.dim
+                    by = 4.0 * n * pp * qq + n * oh * ow * (1 if last.count <= 8 else 2)
+                    codes = self._timed("conv_hash", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv_hash, ex,
+                                        maps, last, view)
                     base = out[s0:s1].view(-1)[(view - 1) * per_view:]
-                    _native.check(lib.ddcca_block_hist(
-                        _native.ptr(codes), codes.element_size(), codes.shape[0], codes.shape[1], codes.shape[2],
-                        plan.n_bits, plan.bh, plan.bw, plan.sh, plan.sw, _native.ptr(base), kind, groups, featlen,
-                        plan.blocks * plan.bins, _native.stream_ptr(ex.stream)), "block_hist")
+                    hb = codes.numel() * codes.element_size() + n * plan.blocks * plan.bins * out.element_size()
+                    self._timed("block_hist", 1, {"kind": "hbm", "bytes": float(hb)}, lambda: _native.check(
+                        lib.ddcca_block_hist(
+                            _native.ptr(codes), codes.element_size(), codes.shape[0], codes.shape[1],
+                            codes.shape[2], plan.n_bits, plan.bh, plan.bw, plan.sh, plan.sw, _native.ptr(base),
+                            kind, groups, featlen, plan.blocks * plan.bins, _native.stream_ptr(ex.stream)),
+                        "block_hist"))
         return out, plan
 
     def expand(self, counts, plan: BlockPlan, enc):

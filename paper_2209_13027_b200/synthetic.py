@@ -57,6 +57,79 @@ def blob_images(n: int, p: int, q: int, classes: int, seed: int = 0, noise: floa
     return out, labels.astype(np.int64)
 
 
+def blob_images_device(n: int, p: int, q: int, classes: int, seed: int = 0, noise: float = 0.02, device="cuda",
+                       start: int = 0, stop: int | None = None, chunk: int = 4096):
+    """Same blob model rendered with torch on ``device`` (benchmark-scale corpora).
+
+    Per-sample parameters come from the same numpy stream as blob_images;
+    noise comes from a torch generator, so pixel values differ from the
+    numpy renderer (both are valid draws of the model). ``start``/``stop``
+    render only a sample range (a rank's shard) with identical parameters.
+    Returns (float32 tensor (stop-start, p, q) on device, int64 numpy labels).
+    """
+    import torch
+
+    stop = n if stop is None else stop
+    rng = np.random.default_rng(seed)
+    ang = 2.0 * np.pi * np.arange(classes) / classes + np.pi / 4.0
+    cy0 = p / 2.0 + (p / 4.0) * np.sin(ang)
+    cx0 = q / 2.0 + (q / 4.0) * np.cos(ang)
+    s = float(min(p, q))
+    labels = np.arange(n) % classes
+    jy = rng.normal(0.0, p / 32.0, n)
+    jx = rng.normal(0.0, q / 32.0, n)
+    amp = rng.uniform(0.75, 1.0, n)
+    f1 = rng.uniform(0.9, 1.1, n)
+    f2 = rng.uniform(0.9, 1.1, n)
+    even = labels % 2 == 0
+    su = np.where(even, s / 6.0 * f1, s / 4.0 * f1)
+    sv = np.where(even, s / 6.0 * f1, s / 10.0 * f2)
+    cy = cy0[labels] + jy
+    cx = cx0[labels] + jx
+    dev = torch.device(device)
+    par = {k: torch.from_numpy(v[start:stop].astype(np.float32)).to(dev)
+           for k, v in dict(cy=cy, cx=cx, amp=amp, su=su, sv=sv, even=even.astype(np.float32)).items()}
+    yy = torch.arange(p, dtype=torch.float32, device=dev)[None, :, None]
+    xx = torch.arange(q, dtype=torch.float32, device=dev)[None, None, :]
+    out = torch.empty((stop - start, p, q), dtype=torch.float32, device=dev)
+    r2 = float(np.sqrt(0.5))
+    for a in range(0, stop - start, chunk):
+        b = min(stop - start, a + chunk)
+        P = {k: v[a:b, None, None] for k, v in par.items()}
+        dy, dx = yy - P["cy"], xx - P["cx"]
+        u = torch.where(P["even"] > 0, dy, (dy + dx) * r2)
+        v = torch.where(P["even"] > 0, dx, (dy - dx) * r2)
+        img = (P["amp"] * torch.exp(-(u * u) / (2 * P["su"] ** 2) - (v * v) / (2 * P["sv"] ** 2))).clamp_(0, 1)
+        if noise > 0:
+            g = torch.Generator(device=dev)
+            g.manual_seed(seed * 1000003 + (start + a))
+            img = (img + noise * torch.randn(img.shape, generator=g, device=dev)).clamp_(0, 1)
+        out[a:b] = img
+    return out, labels[start:stop].astype(np.int64)
+
+
+def second_view_device(view1, kind: str, seed: int = 1, noise: float = 0.02):
+    """Torch version of second_view for 'pair' and 'lbp' (device tensors)."""
+    import torch
+
+    if kind == "lbp":
+        n, p, q = view1.shape
+        pad = torch.zeros((n, p + 2, q + 2), dtype=torch.float32, device=view1.device)
+        pad[:, 1:-1, 1:-1] = view1
+        code = torch.zeros_like(view1)
+        for bit, (dy, dx) in enumerate(_LBP_OFFSETS):
+            code += float(1 << bit) * (pad[:, 1 + dy:1 + dy + p, 1 + dx:1 + dx + q] > view1).float()
+        return code / 255.0
+    if kind in ("pair", "channel"):
+        sm = view1.clone()
+        sm[:, 1:-1, 1:-1] = (view1[:, :-2, 1:-1] + view1[:, 2:, 1:-1] + view1[:, 1:-1, :-2] + view1[:, 1:-1, 2:]
+                             + view1[:, 1:-1, 1:-1]) / 5.0
+        g = torch.Generator(device=view1.device)
+        g.manual_seed(seed)
+        return (0.8 * sm ** 1.5 + noise * torch.randn(view1.shape, generator=g, device=view1.device)).clamp_(0, 1)
+    raise ValueError(f"unknown second-view kind {kind!r}")
+
+
 def lbp_maps(imgs: np.ndarray) -> np.ndarray:
     """8-neighbour LBP / 255 of each image (views.py:41-58): strict >, clockwise from top-left, zero pad."""
     x = np.asarray(imgs, dtype=np.float64)
