@@ -37,46 +37,59 @@ struct ConvArgs {
   void* out;          // float (n_maps, count, oh, ow) or codes (n_maps, oh, ow)
 };
 
+// Tile row stride (floats) of the staged input: multiple of 4 so float4 loads stay aligned.
+__host__ __device__ inline int conv_tile_width(int ow, int l2, int px) {
+  const int G = (ow + px - 1) / px;
+  return ((G * px + l2 + 3) + 3) / 4 * 4;
+}
+
+// Centered conv as an uncentered conv with zero-mean taps: for every window
+//   sum_k W_k (x_k - m) = sum_k (W_k - mean(W)) (x_k - c)   for any constant c,
+// so the kernel never forms window means. c is a per-thread constant (a pixel
+// of the thread's own windows) that removes the DC part before the float32 sums.
 // MODE 0: write float responses; MODE 1: write u8 codes; MODE 2: write u16 codes
 template <int NF, int PX, int L2, int MODE>
 __global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A) {
-  extern __shared__ float smf[];
+  extern __shared__ __align__(16) float smf[];
   const int l2 = L2 > 0 ? L2 : A.l2;
   const int d = A.l1 * l2;
-  float* wsm = smf;                       // [d][NF]
-  float* swm = wsm + d * NF;              // [NF]
-  float* tile = swm + NF;                 // [rows][Wt]
+  float* wsm = smf;                       // [d][NF] zero-mean taps when centering
+  float* tile = wsm + d * NF;             // [rows][Wt]
   const int G = (A.ow + PX - 1) / PX;     // thread groups per output row
-  const int items_per_block = CONV_THREADS;
   const int64_t per_map = (int64_t)A.oh * G;
-  const int blocks_per_map = (int)((per_map + items_per_block - 1) / items_per_block);
+  const int blocks_per_map = (int)((per_map + CONV_THREADS - 1) / CONV_THREADS);
   const int64_t m = blockIdx.x / blocks_per_map;
   const int bi = blockIdx.x % blocks_per_map;
   if (m >= A.n_maps) return;
-  const int64_t i0 = (int64_t)bi * items_per_block;
+  const int64_t i0 = (int64_t)bi * CONV_THREADS;
   const int u_first = (int)(i0 / G);
-  const int u_last = (int)(min(per_map, i0 + items_per_block) - 1) / G;
+  const int u_last = (int)(min(per_map, i0 + CONV_THREADS) - 1) / G;
   const int rows = u_last - u_first + A.l1;
-  const int Wt = A.ow + l2 - 1 + PX;  // staged padded columns (slack for the last group)
-  // filters -> smem (zero-padded to NF), per-filter tap sums
-  for (int e = threadIdx.x; e < d * NF; e += blockDim.x) {
-    const int k = e / NF, g = e % NF;
-    wsm[e] = g < A.count ? A.pack[k * A.count + g] : 0.f;
-  }
+  const int Wt = conv_tile_width(A.ow, l2, PX);
+  // taps -> smem; zero-mean per filter when centering (mean in float64)
+  __shared__ float wmean[NF];
   if (threadIdx.x < NF) {
     double s = 0.0;
-    if ((int)threadIdx.x < A.count)
+    if (A.center && (int)threadIdx.x < A.count)
       for (int k = 0; k < d; ++k) s += (double)A.pack[k * A.count + threadIdx.x];
-    swm[threadIdx.x] = (float)s;
+    wmean[threadIdx.x] = (float)(s / d);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < d * NF; e += blockDim.x) {
+    const int k = e / NF, g = e % NF;
+    wsm[e] = g < A.count ? (float)((double)A.pack[k * A.count + g] - (double)wmean[g]) : 0.f;
   }
   // input tile: padded rows [u_first, u_first + rows), padded cols [0, Wt)
   const float* img = A.in + m * (int64_t)A.p * A.q;
-  for (int e = threadIdx.x; e < rows * Wt; e += blockDim.x) {
-    const int r = e / Wt, c = e - r * Wt;
-    const int i = u_first + r - A.top, j = c - A.left;
-    float v = 0.f;
-    if (i >= 0 && i < A.p && j >= 0 && j < A.q) v = __ldg(img + (int64_t)i * A.q + j);
-    tile[e] = v;
+  for (int r = threadIdx.x >> 5; r < rows; r += CONV_THREADS / 32) {
+    const int i = u_first + r - A.top;
+    const bool rok = i >= 0 && i < A.p;
+    for (int c = threadIdx.x & 31; c < Wt; c += 32) {
+      const int j = c - A.left;
+      float v = 0.f;
+      if (rok && j >= 0 && j < A.q) v = __ldg(img + (int64_t)i * A.q + j);
+      tile[r * Wt + c] = v;
+    }
   }
   __syncthreads();
   const int64_t item = i0 + threadIdx.x;
@@ -84,30 +97,29 @@ __global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A) {
   const int u = (int)(item / G);
   const int v0 = (int)(item % G) * PX;
   const int r0 = u - u_first;
-  float c = 0.f;
-  if (A.center) c = tile[(r0 + (A.l1 - 1) / 2) * Wt + v0 + (l2 - 1) / 2];
+  const float c = A.center ? tile[(r0 + (A.l1 - 1) / 2) * Wt + v0 + (l2 - 1) / 2] : 0.f;
   float acc[PX][NF];
-  float bs[PX];
 #pragma unroll
-  for (int j = 0; j < PX; ++j) {
-    bs[j] = 0.f;
+  for (int j = 0; j < PX; ++j)
 #pragma unroll
     for (int g = 0; g < NF; ++g) acc[j][g] = 0.f;
-  }
   for (int a = 0; a < A.l1; ++a) {
     const float* row = tile + (r0 + a) * Wt + v0;
     if constexpr (L2 > 0) {
-      float x[PX + L2 - 1];
+      constexpr int NX = PX + L2 - 1;
+      float x[(NX + 3) / 4 * 4];
+      if constexpr (PX % 4 == 0) {
 #pragma unroll
-      for (int t = 0; t < PX + L2 - 1; ++t) x[t] = row[t] - c;
-      if (A.center) {
-#pragma unroll
-        for (int j = 0; j < PX; ++j) {
-          float s = 0.f;
-#pragma unroll
-          for (int b = 0; b < L2; ++b) s += x[j + b];
-          bs[j] += s;
+        for (int t4 = 0; t4 < (NX + 3) / 4; ++t4) {
+          const float4 v = *reinterpret_cast<const float4*>(row + 4 * t4);
+          x[4 * t4 + 0] = v.x - c;
+          x[4 * t4 + 1] = v.y - c;
+          x[4 * t4 + 2] = v.z - c;
+          x[4 * t4 + 3] = v.w - c;
         }
+      } else {
+#pragma unroll
+        for (int t = 0; t < NX; ++t) x[t] = row[t] - c;
       }
 #pragma unroll
       for (int b = 0; b < L2; ++b) {
@@ -128,10 +140,7 @@ __global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A) {
       for (int b = 0; b < l2; ++b) {
         float xv[PX];
 #pragma unroll
-        for (int j = 0; j < PX; ++j) {
-          xv[j] = row[j + b] - c;
-          bs[j] += xv[j];
-        }
+        for (int j = 0; j < PX; ++j) xv[j] = row[j + b] - c;
         const float4* wp = reinterpret_cast<const float4*>(wsm + (a * l2 + b) * NF);
 #pragma unroll
         for (int g4 = 0; g4 < NF / 4; ++g4) {
@@ -147,25 +156,75 @@ __global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A) {
       }
     }
   }
-  const float invd = 1.0f / (float)d;
   const int64_t plane = (int64_t)A.oh * A.ow;
+  // full, aligned groups: vector stores (each warp writes contiguous rows per filter)
+  if constexpr (PX % 4 == 0) {
+    if (v0 + PX <= A.ow && (A.ow & 3) == 0) {
+      if constexpr (MODE == 0) {
+        float* o = static_cast<float*>(A.out) + (m * A.count) * plane + (int64_t)u * A.ow + v0;
+#pragma unroll
+        for (int g = 0; g < NF; ++g)
+          if (g < A.count) {
+#pragma unroll
+            for (int j4 = 0; j4 < PX / 4; ++j4)
+              *reinterpret_cast<float4*>(o + g * plane + 4 * j4) =
+                  make_float4(acc[4 * j4][g], acc[4 * j4 + 1][g], acc[4 * j4 + 2][g], acc[4 * j4 + 3][g]);
+          }
+      } else if constexpr (MODE == 1) {
+        uint32_t wds[PX / 4];
+#pragma unroll
+        for (int j4 = 0; j4 < PX / 4; ++j4) {
+          uint32_t wv = 0;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            unsigned code = 0;
+#pragma unroll
+            for (int g = 0; g < NF; ++g)
+              if (g < A.count && acc[4 * j4 + jj][g] > 0.f) code |= 1u << g;
+            wv |= code << (8 * jj);
+          }
+          wds[j4] = wv;
+        }
+        uint8_t* o = static_cast<uint8_t*>(A.out) + m * plane + (int64_t)u * A.ow + v0;
+        if constexpr (PX == 8)
+          *reinterpret_cast<uint2*>(o) = make_uint2(wds[0], wds[1]);
+        else
+#pragma unroll
+          for (int j4 = 0; j4 < PX / 4; ++j4) *reinterpret_cast<uint32_t*>(o + 4 * j4) = wds[j4];
+      } else {
+#pragma unroll
+        for (int j4 = 0; j4 < PX / 4; ++j4) {
+          uint32_t lo = 0, hi = 0;
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            unsigned code = 0;
+#pragma unroll
+            for (int g = 0; g < NF; ++g)
+              if (g < A.count && acc[4 * j4 + jj][g] > 0.f) code |= 1u << g;
+            if (jj < 2) lo |= code << (16 * jj);
+            else hi |= code << (16 * (jj - 2));
+          }
+          *reinterpret_cast<uint2*>(static_cast<uint16_t*>(A.out) + m * plane + (int64_t)u * A.ow + v0 + 4 * j4) =
+              make_uint2(lo, hi);
+        }
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < PX; ++j) {
     const int v = v0 + j;
     if (v >= A.ow) break;
-    const float mc = A.center ? bs[j] * invd : 0.f;
     if constexpr (MODE == 0) {
       float* o = static_cast<float*>(A.out) + (m * A.count) * plane + (int64_t)u * A.ow + v;
 #pragma unroll
       for (int g = 0; g < NF; ++g)
-        if (g < A.count) o[g * plane] = A.center ? fmaf(-swm[g], mc, acc[j][g]) : acc[j][g];
+        if (g < A.count) o[g * plane] = acc[j][g];
     } else {
       unsigned code = 0;
 #pragma unroll
-      for (int g = 0; g < NF; ++g) {
-        const float r = A.center ? fmaf(-swm[g], mc, acc[j][g]) : acc[j][g];
-        if (g < A.count && r > 0.f) code |= 1u << g;
-      }
+      for (int g = 0; g < NF; ++g)
+        if (g < A.count && acc[j][g] > 0.f) code |= 1u << g;
       if constexpr (MODE == 1)
         static_cast<uint8_t*>(A.out)[m * plane + (int64_t)u * A.ow + v] = (uint8_t)code;
       else
@@ -331,10 +390,10 @@ static int launch_s1(const ConvArgs& A, cudaStream_t st) {
   const int64_t per_map = (int64_t)A.oh * G;
   const int bpm = (int)((per_map + CONV_THREADS - 1) / CONV_THREADS);
   const int max_rows = (CONV_THREADS + G - 1) / G + 1 + A.l1;
-  const size_t smem = sizeof(float) * ((size_t)A.l1 * l2 * NF + NF + (size_t)max_rows * (A.ow + l2 - 1 + PX));
+  const size_t smem = sizeof(float) * ((size_t)A.l1 * l2 * NF + (size_t)max_rows * conv_tile_width(A.ow, l2, PX));
   const int64_t nblocks = (int64_t)bpm * A.n_maps;
   if (nblocks > 0x7fffffffLL) return fail(DDCCA_ECONFIG, "conv: too many maps in one call");
-  if (smem > 220 * 1024) return fail(DDCCA_ECONFIG, "conv: map row too wide for shared-memory staging");
+  if (smem > 200 * 1024) return fail(DDCCA_ECONFIG, "conv: map row too wide for shared-memory staging");
 #define DDCCA_CONV_L2(N)                                                                                   \
   case N:                                                                                                  \
     cudaFuncSetAttribute(conv_s1_kernel<NF, PX, N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
@@ -354,7 +413,7 @@ template <int MODE>
 static int launch_conv(const ConvArgs& A, int stride, cudaStream_t st) {
   if (A.n_maps == 0) return DDCCA_OK;
   if (stride == 1) {
-    if (A.count <= 8) return launch_s1<8, 4, MODE>(A, st);
+    if (A.count <= 8) return launch_s1<8, 8, MODE>(A, st);
     if (A.count <= 16) return launch_s1<16, 4, MODE>(A, st);
     if (A.count <= 32) return launch_s1<32, 2, MODE>(A, st);
     if (A.count <= 64 && MODE == 0) return launch_s1<64, 1, MODE>(A, st);

@@ -40,7 +40,7 @@ namespace ddcca {
 
 constexpr int KDX = 3;       // dx lags per thread
 constexpr int TILE_X = 32;   // first-pixel columns per block (one per lane)
-constexpr int SLAB_Y = 32;   // max first-pixel rows per interior task
+constexpr int STAGE_ROWS = 48;  // staged rows per cp.async stage (all maps of the stage)
 constexpr int MAPS_PER_SPLIT = 128;
 constexpr int MAX_LAG_L = 12;  // lag path for windows up to 12 x 12
 
@@ -83,7 +83,7 @@ struct RecInfo {
 struct Plan {
   Geo g;
   Zones z;
-  int nrz, ncz, G, NDX, NDF;
+  int nrz, ncz, G, NDX, NDF, slab;
   std::vector<Task> tasks;
   std::vector<RecInfo> recs;
   std::vector<int> lane_slot;  // per task * 32 + lane -> record offset within task, or -1 (big zone)
@@ -106,6 +106,8 @@ static void make_plan(const Geo& g, Plan* P) {
   P->G = (2 * g.l2 - 1 + KDX - 1) / KDX;
   P->NDX = P->G * KDX;
   P->NDF = g.l1 * P->NDX;
+  // one stage stages at most PF_ROWS rows per warp: slab + halo must fit
+  P->slab = 32;
   P->tasks.clear();
   P->recs.clear();
   P->lane_slot.clear();
@@ -115,8 +117,8 @@ static void make_plan(const Geo& g, Plan* P) {
     int rz = P->z.rz_of_y[y];
     int y_end = y;
     while (y_end < g.Hp && P->z.rz_of_y[y_end] == rz) ++y_end;
-    for (int ys = y; ys < y_end; ys += SLAB_Y) {
-      int ye = std::min(y_end, ys + SLAB_Y);
+    for (int ys = y; ys < y_end; ys += P->slab) {
+      int ye = std::min(y_end, ys + P->slab);
       for (int x0 = 0; x0 < g.Wp; x0 += TILE_X) {
         Task t;
         t.y0 = ys; t.y1 = ye; t.x0 = x0; t.rz = rz; t.rec0 = nrec; t.nrec = 0;
@@ -152,7 +154,7 @@ static void make_plan(const Geo& g, Plan* P) {
 // lag_zone_kernel
 // ----------------------------------------------------------------------------
 struct TaskDev {
-  int y0, y1, x0, rec0;
+  int y0, y1, x0, rec0, mb;  // rows [y0, y1), tile column x0, first record, maps per stage
 };
 
 struct LagArgs {
@@ -164,9 +166,52 @@ struct LagArgs {
   int p, q, top, left, Wp, l2, G, NDX, NDF, nrec, nsplit, nbatch;
 };
 
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 4 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// Sum over rows [0, nrows) of one staged map tile (float64, row stride tc) of
+// own * partner for the L1 x KDX lags of this thread. Rows are processed in
+// whole ring turns of L1; rows >= nrows are masked through the own value
+// (their staged data is still valid partner data for earlier rows).
+template <int L1, bool SKIP0>
+__device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int tc, int nrows, int cown, int cpart,
+                                               double (&acc)[L1][KDX]) {
+  double ring[L1][KDX];
+  const double* pp = t + cpart;
+#pragma unroll
+  for (int q = 0; q < L1 - 1; ++q)
+#pragma unroll
+    for (int k = 0; k < KDX; ++k) ring[q][k] = pp[q * tc + k];
+  pp += (L1 - 1) * tc;
+  const double* po = t + cown;
+  for (int r0 = 0; r0 < nrows; r0 += L1) {
+#pragma unroll
+    for (int u = 0; u < L1; ++u) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int snew = (u + L1 - 1) % L1;
+#pragma unroll
+      for (int k = 0; k < KDX; ++k) ring[snew][k] = pp[k];
+      pp += tc;
+      double own = *po;
+      po += tc;
+      own = (r0 + u < nrows) ? own : 0.0;
+#pragma unroll
+      for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy)
+#pragma unroll
+        for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, ring[(u + dy) % L1][k], acc[dy][k]);
+    }
+  }
+}
+
 template <int L1>
-__global__ void __launch_bounds__(256) lag_zone_kernel(LagArgs A) {
-  extern __shared__ double tile[];
+__global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArgs A) {
+  extern __shared__ __align__(16) double smem_d[];
   const int task = blockIdx.x;
   const int split = blockIdx.y;
   const int bv = blockIdx.z;  // batch * 2 + view
@@ -174,17 +219,45 @@ __global__ void __launch_bounds__(256) lag_zone_kernel(LagArgs A) {
   const TaskDev T = A.tasks[task];
   const int lane = threadIdx.x & 31;
   const int grp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
   const int nrows = T.y1 - T.y0;
-  const int tr = nrows + L1 - 1;                  // staged rows
-  const int tc = TILE_X + A.NDX - 1;              // staged cols: [x0-(l2-1), x0-(l2-1)+tc)
+  const int nrows_pad = (nrows + L1 - 1) / L1 * L1;
+  const int tr = nrows_pad + L1 - 1;              // staged rows per map (zero beyond the map)
+  const int tc = TILE_X + A.NDX - 1;              // staged cols: [x0-(l2-1), x0-(l2-1)+tc), tc <= 64
+  const int tile_elems = tr * tc;
+  const int mb = T.mb;
+  const int stage_elems = mb * tile_elems;
+  double* f64 = smem_d;                                             // [mb][tr][tc] float64
+  float* raw = reinterpret_cast<float*>(smem_d + stage_elems);      // 2 x [mb][tr][tc] float32
   const int xs = T.x0 - (A.l2 - 1);
   const int64_t m_begin = A.batch_off[batch];
   const int64_t m_end = A.batch_off[batch + 1];
   const int64_t per = (m_end - m_begin + A.nsplit - 1) / A.nsplit;
   const int64_t ma = m_begin + (int64_t)split * per;
-  const int64_t mb = min(m_end, ma + per);
+  const int64_t mbnd = min(m_end, ma + per);
   const float* src = view == 0 ? A.maps[0] : A.maps[1];
-  const int plane = A.p * A.q;
+  const int64_t plane = (int64_t)A.p * A.q;
+
+  // cp.async staging: warp w copies flat rows fr = w, w + nwarps, ... (fr = j * tr + r),
+  // lanes copy tile columns lane and lane + 32; out-of-image elements are zero-filled.
+  auto issue = [&](int64_t ms, float* dst) {
+    for (int fr = grp; fr < mb * tr; fr += nwarps) {
+      const int j = fr / tr, r = fr - j * tr;
+      const int img_row = T.y0 + r - A.top;
+      const bool rok = img_row >= 0 && img_row < A.p && (r < nrows + L1 - 1) && (ms + j < mbnd);
+      const float* rowp = src + (ms + j) * plane + (int64_t)img_row * A.q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        if (c < tc) {
+          const int col = xs + c - A.left;
+          const bool ok = rok && col >= 0 && col < A.q;
+          cp_async4(dst + fr * tc + c, ok ? rowp + col : src, ok);
+        }
+      }
+    }
+    cp_async_commit();
+  };
 
   double acc[L1][KDX];
 #pragma unroll
@@ -194,48 +267,35 @@ __global__ void __launch_bounds__(256) lag_zone_kernel(LagArgs A) {
 
   const int cown = lane + (A.l2 - 1);  // own column inside the tile
   const int cpart = lane + grp * KDX;  // partner column of k = 0
+  // groups whose dx are all negative skip the dy = 0 lag (canonical half-plane only)
+  const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
 
-  for (int64_t m = ma; m < mb; ++m) {
-    const float* img = src + m * (int64_t)plane;
+  if (ma < mbnd) issue(ma, raw);
+  int s = 0;
+  for (int64_t ms = ma; ms < mbnd; ms += mb, ++s) {
+    float* cur = raw + (s & 1) * stage_elems;
+    if (ms + mb < mbnd)
+      issue(ms + mb, raw + ((s + 1) & 1) * stage_elems);
+    else
+      cp_async_commit();  // keep one group per iteration for wait_group 1
+    cp_async_wait1();
+    __syncthreads();  // stage s visible to all; previous compute on f64 finished
+    for (int e = threadIdx.x; e < stage_elems; e += blockDim.x) f64[e] = (double)cur[e];
     __syncthreads();
-    for (int e = threadIdx.x; e < tr * tc; e += blockDim.x) {
-      int r = e / tc, c = e - r * tc;
-      int i = T.y0 + r - A.top, j = xs + c - A.left;
-      float v = 0.f;
-      if (i >= 0 && i < A.p && j >= 0 && j < A.q) v = __ldg(img + (int64_t)i * A.q + j);
-      tile[e] = (double)v;
-    }
-    __syncthreads();
-    if (grp >= A.G) continue;
-    double ring[L1][KDX];
-#pragma unroll
-    for (int s = 0; s < L1 - 1; ++s)
-#pragma unroll
-      for (int k = 0; k < KDX; ++k) ring[s][k] = tile[s * tc + cpart + k];
-    for (int r0 = 0; r0 < nrows; r0 += L1) {
-#pragma unroll
-      for (int u = 0; u < L1; ++u) {
-        const int r = r0 + u;
-        if (r < nrows) {
-          const int snew = (u + L1 - 1) % L1;
-#pragma unroll
-          for (int k = 0; k < KDX; ++k) ring[snew][k] = tile[(r + L1 - 1) * tc + cpart + k];
-          const double own = tile[r * tc + cown];
-#pragma unroll
-          for (int dy = 0; dy < L1; ++dy)
-#pragma unroll
-            for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, ring[(u + dy) % L1][k], acc[dy][k]);
-        }
-      }
+    const int nm = (int)min((int64_t)mb, mbnd - ms);
+    for (int j = 0; j < nm; ++j) {
+      if (skip0)
+        lag_accumulate<L1, true>(f64 + j * tile_elems, tc, nrows, cown, cpart, acc);
+      else
+        lag_accumulate<L1, false>(f64 + j * tile_elems, tc, nrows, cown, cpart, acc);
     }
   }
-  if (grp >= A.G) return;
   // lanes outside the map's padded width hold zeros already (tile zero-filled)
   const int slot = A.lane_slot[task * TILE_X + lane];
   const int x = T.x0 + lane;
   const bool in_big = (slot < 0) && (x < A.Wp);
   double* out = A.rec + (((int64_t)batch * 2 + view) * A.nsplit + split) * (int64_t)A.nrec * A.NDF;
-  // big-zone record index is rec0 (the task's first record) when present
+  const int any_big = __any_sync(0xffffffffu, in_big);
 #pragma unroll
   for (int dy = 0; dy < L1; ++dy)
 #pragma unroll
@@ -243,7 +303,6 @@ __global__ void __launch_bounds__(256) lag_zone_kernel(LagArgs A) {
       const int lag = dy * A.NDX + grp * KDX + k;
       double v = in_big ? acc[dy][k] : 0.0;
       v = warp_sum(v);
-      const int any_big = __any_sync(0xffffffffu, in_big);
       if (lane == 0 && any_big) out[(int64_t)T.rec0 * A.NDF + lag] = v;
       if (slot >= 0) out[(int64_t)(T.rec0 + slot) * A.NDF + lag] = acc[dy][k];
     }
@@ -351,37 +410,32 @@ struct RectArgs {
 
 __global__ void rect_sums_kernel(RectArgs A) {
   extern __shared__ double sm[];
-  double* rowz = sm;                          // [Hp][ncz]
-  double* Zp = sm + (int64_t)A.Hp * A.ncz;    // [nrz][ncz]
-  double* R = Zp + A.nrz * A.ncz;             // [d]
+  double* colz = sm;                            // [nrz][Wp]: per column, sum over each row zone
+  double* Zp = sm + (int64_t)A.nrz * A.Wp;      // [nrz][ncz]
+  double* R = Zp + A.nrz * A.ncz;               // [d]
   const int64_t m = blockIdx.x;
   const int view = blockIdx.y;
   const float* img = (view == 0 ? A.maps[0] : A.maps[1]) + m * (int64_t)A.p * A.q;
-  for (int e = threadIdx.x; e < A.Hp * A.ncz; e += blockDim.x) rowz[e] = 0.0;
-  __syncthreads();
-  // one thread per padded row: column-zone sums of that row (pads are zero)
-  for (int y = threadIdx.x; y < A.Hp; y += blockDim.x) {
-    const int i = y - A.top;
-    if (i < 0 || i >= A.p) continue;
-    double cur = 0.0;
-    int czc = A.cz_of_x[A.left];
-    for (int j = 0; j < A.q; ++j) {
-      const int cz = A.cz_of_x[j + A.left];
-      if (cz != czc) {
-        rowz[y * A.ncz + czc] += cur;
-        cur = 0.0;
-        czc = cz;
+  // thread per padded column; rows walked zone by zone (coalesced across threads)
+  for (int x = threadIdx.x; x < A.Wp; x += blockDim.x) {
+    const int j = x - A.left;
+    const bool cok = j >= 0 && j < A.q;
+    int y = 0;
+    for (int rz = 0; rz < A.nrz; ++rz) {
+      double s = 0.0;
+      for (; y < A.Hp && A.rz_of_y[y] == rz; ++y) {
+        const int i = y - A.top;
+        if (cok && i >= 0 && i < A.p) s += (double)__ldg(img + (int64_t)i * A.q + j);
       }
-      cur += (double)img[(int64_t)i * A.q + j];
+      colz[rz * A.Wp + x] = s;
     }
-    rowz[y * A.ncz + czc] += cur;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < A.nrz * A.ncz; e += blockDim.x) {
     const int rz = e / A.ncz, cz = e % A.ncz;
     double s = 0.0;
-    for (int y = 0; y < A.Hp; ++y)
-      if (A.rz_of_y[y] == rz) s += rowz[y * A.ncz + cz];
+    for (int x = 0; x < A.Wp; ++x)
+      if (A.cz_of_x[x] == cz) s += colz[rz * A.Wp + x];
     Zp[e] = s;
   }
   __syncthreads();
@@ -735,7 +789,14 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     const Plan& P = L.P;
     // upload plan tables (small; pageable H2D copies are staged by the driver)
     std::vector<TaskDev> td(P.tasks.size());
-    for (size_t t = 0; t < P.tasks.size(); ++t) td[t] = {P.tasks[t].y0, P.tasks[t].y1, P.tasks[t].x0, P.tasks[t].rec0};
+    size_t max_stage = 1;
+    for (size_t t = 0; t < P.tasks.size(); ++t) {
+      const int nr = P.tasks[t].y1 - P.tasks[t].y0;
+      const int tr = (nr + g.l1 - 1) / g.l1 * g.l1 + g.l1 - 1;
+      const int mb = std::max(1, std::min(8, STAGE_ROWS / tr));
+      td[t] = {P.tasks[t].y0, P.tasks[t].y1, P.tasks[t].x0, P.tasks[t].rec0, mb};
+      max_stage = std::max(max_stage, (size_t)mb * tr);
+    }
     const int nzone = P.nrz * P.ncz;
     std::vector<int> zoff(nzone + 1, 0), zlist(P.nrec);
     for (int r = 0; r < P.nrec; ++r) zoff[P.recs[r].rz * P.ncz + P.recs[r].cz + 1]++;
@@ -772,14 +833,15 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     A.rec = reinterpret_cast<double*>(w + L.off_rec);
     A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
     A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.nbatch = n_batches;
-    const int maxrows = SLAB_Y + g.l1 - 1;
-    const size_t smem = sizeof(double) * maxrows * (TILE_X + P.NDX - 1);
+    // float64 compute tile + two float32 cp.async buffers
+    const size_t smem = (sizeof(double) + 2 * sizeof(float)) * max_stage * (TILE_X + P.NDX - 1);
     dim3 grid((unsigned)P.tasks.size(), (unsigned)L.nsplit, (unsigned)(n_batches * 2));
     dim3 block(32 * P.G);
     switch (g.l1) {
 #define DDCCA_LAG_CASE(N)                                                                          \
   case N:                                                                                          \
     cudaFuncSetAttribute(lag_zone_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(lag_zone_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);    \
     lag_zone_kernel<N><<<grid, block, smem, st>>>(A);                                              \
     break;
       DDCCA_LAG_CASE(1) DDCCA_LAG_CASE(2) DDCCA_LAG_CASE(3) DDCCA_LAG_CASE(4) DDCCA_LAG_CASE(5)
@@ -815,9 +877,11 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       R.rz_of_y = rz_of_y; R.cz_of_x = cz_of_x; R.rz_lo = rz_lo; R.rz_hi = rz_hi; R.cz_lo = cz_lo; R.cz_hi = cz_hi;
       R.n_maps = n_maps; R.p = g.p; R.q = g.q; R.top = g.top; R.left = g.left; R.Hp = g.Hp; R.Wp = g.Wp;
       R.nrz = P.nrz; R.ncz = P.ncz; R.l1 = g.l1; R.l2 = g.l2; R.d = g.d; R.center = center;
-      const size_t sm = sizeof(double) * ((size_t)g.Hp * P.ncz + (size_t)P.nrz * P.ncz + g.d);
+      const size_t sm = sizeof(double) * ((size_t)P.nrz * g.Wp + (size_t)P.nrz * P.ncz + g.d);
+      if (sm > 200 * 1024) return fail(DDCCA_ECONFIG, "moments: map too wide for the window-sum kernel");
       cudaFuncSetAttribute(rect_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      rect_sums_kernel<<<dim3((unsigned)n_maps, 2), 128, sm, st>>>(R);
+      const int rthreads = std::min(512, (g.Wp + 31) / 32 * 32);
+      rect_sums_kernel<<<dim3((unsigned)n_maps, 2), rthreads, sm, st>>>(R);
       DDCCA_TRY(check_launch("moments: rect_sums"));
       batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(R.out, map_label, A.batch_off, n_maps, g.d,
                                                                  class_count, plen, cols_per_map, partials);
