@@ -107,7 +107,7 @@ static void make_plan(const Geo& g, Plan* P) {
   P->NDX = P->G * KDX;
   P->NDF = g.l1 * P->NDX;
   // one stage stages at most PF_ROWS rows per warp: slab + halo must fit
-  P->slab = 32;
+  P->slab = g.l1 * std::max(1, 32 / g.l1);  // whole ring turns
   P->tasks.clear();
   P->recs.clear();
   P->lane_slot.clear();
@@ -209,6 +209,22 @@ __device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int
   }
 }
 
+// Tasks shorter than one ring turn (the single border rows): direct partner loads.
+template <int L1>
+__device__ __forceinline__ void lag_accumulate_short(const double* __restrict__ t, int tc, int nrows, int cown,
+                                                     int cpart, bool skip0, double (&acc)[L1][KDX]) {
+  for (int r = 0; r < nrows; ++r) {
+    const double own = t[r * tc + cown];
+    const double* pp = t + r * tc + cpart;
+#pragma unroll
+    for (int dy = 0; dy < L1; ++dy) {
+      if (dy == 0 && skip0) continue;
+#pragma unroll
+      for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, pp[dy * tc + k], acc[dy][k]);
+    }
+  }
+}
+
 template <int L1>
 __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArgs A) {
   extern __shared__ __align__(16) double smem_d[];
@@ -221,7 +237,8 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   const int grp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int nrows = T.y1 - T.y0;
-  const int nrows_pad = (nrows + L1 - 1) / L1 * L1;
+  const bool short_task = nrows < L1;
+  const int nrows_pad = short_task ? nrows : (nrows + L1 - 1) / L1 * L1;
   const int tr = nrows_pad + L1 - 1;              // staged rows per map (zero beyond the map)
   const int tc = TILE_X + A.NDX - 1;              // staged cols: [x0-(l2-1), x0-(l2-1)+tc), tc <= 64
   const int tile_elems = tr * tc;
@@ -284,7 +301,9 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
     __syncthreads();
     const int nm = (int)min((int64_t)mb, mbnd - ms);
     for (int j = 0; j < nm; ++j) {
-      if (skip0)
+      if (short_task)
+        lag_accumulate_short<L1>(f64 + j * tile_elems, tc, nrows, cown, cpart, skip0, acc);
+      else if (skip0)
         lag_accumulate<L1, true>(f64 + j * tile_elems, tc, nrows, cown, cpart, acc);
       else
         lag_accumulate<L1, false>(f64 + j * tile_elems, tc, nrows, cown, cpart, acc);
@@ -792,7 +811,7 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     size_t max_stage = 1;
     for (size_t t = 0; t < P.tasks.size(); ++t) {
       const int nr = P.tasks[t].y1 - P.tasks[t].y0;
-      const int tr = (nr + g.l1 - 1) / g.l1 * g.l1 + g.l1 - 1;
+      const int tr = (nr < g.l1 ? nr : (nr + g.l1 - 1) / g.l1 * g.l1) + g.l1 - 1;
       const int mb = std::max(1, std::min(8, STAGE_ROWS / tr));
       td[t] = {P.tasks[t].y0, P.tasks[t].y1, P.tasks[t].x0, P.tasks[t].rec0, mb};
       max_stage = std::max(max_stage, (size_t)mb * tr);
