@@ -48,55 +48,17 @@ __host__ __device__ inline int conv_tile_width(int ow, int l2, int px) {
 // so the kernel never forms window means. c is a per-thread constant (a pixel
 // of the thread's own windows) that removes the DC part before the float32 sums.
 // MODE 0: write float responses; MODE 1: write u8 codes; MODE 2: write u16 codes
+__device__ __forceinline__ void cp_async4z(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0));
+}
+
+// One output strip (PX pixels x NF filters) of one map from a staged tile.
 template <int NF, int PX, int L2, int MODE>
-__global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A) {
-  extern __shared__ __align__(16) float smf[];
+__device__ __forceinline__ void conv_strip(const ConvArgs& A, const float* __restrict__ wsm,
+                                           const float* __restrict__ tile, int Wt, int64_t m, int u, int v0,
+                                           int r0) {
   const int l2 = L2 > 0 ? L2 : A.l2;
-  const int d = A.l1 * l2;
-  float* wsm = smf;                       // [d][NF] zero-mean taps when centering
-  float* tile = wsm + d * NF;             // [rows][Wt]
-  const int G = (A.ow + PX - 1) / PX;     // thread groups per output row
-  const int64_t per_map = (int64_t)A.oh * G;
-  const int blocks_per_map = (int)((per_map + CONV_THREADS - 1) / CONV_THREADS);
-  const int64_t m = blockIdx.x / blocks_per_map;
-  const int bi = blockIdx.x % blocks_per_map;
-  if (m >= A.n_maps) return;
-  const int64_t i0 = (int64_t)bi * CONV_THREADS;
-  const int u_first = (int)(i0 / G);
-  const int u_last = (int)(min(per_map, i0 + CONV_THREADS) - 1) / G;
-  const int rows = u_last - u_first + A.l1;
-  const int Wt = conv_tile_width(A.ow, l2, PX);
-  // taps -> smem; zero-mean per filter when centering (mean in float64)
-  __shared__ float wmean[NF];
-  if (threadIdx.x < NF) {
-    double s = 0.0;
-    if (A.center && (int)threadIdx.x < A.count)
-      for (int k = 0; k < d; ++k) s += (double)A.pack[k * A.count + threadIdx.x];
-    wmean[threadIdx.x] = (float)(s / d);
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < d * NF; e += blockDim.x) {
-    const int k = e / NF, g = e % NF;
-    wsm[e] = g < A.count ? (float)((double)A.pack[k * A.count + g] - (double)wmean[g]) : 0.f;
-  }
-  // input tile: padded rows [u_first, u_first + rows), padded cols [0, Wt)
-  const float* img = A.in + m * (int64_t)A.p * A.q;
-  for (int r = threadIdx.x >> 5; r < rows; r += CONV_THREADS / 32) {
-    const int i = u_first + r - A.top;
-    const bool rok = i >= 0 && i < A.p;
-    for (int c = threadIdx.x & 31; c < Wt; c += 32) {
-      const int j = c - A.left;
-      float v = 0.f;
-      if (rok && j >= 0 && j < A.q) v = __ldg(img + (int64_t)i * A.q + j);
-      tile[r * Wt + c] = v;
-    }
-  }
-  __syncthreads();
-  const int64_t item = i0 + threadIdx.x;
-  if (item >= per_map) return;
-  const int u = (int)(item / G);
-  const int v0 = (int)(item % G) * PX;
-  const int r0 = u - u_first;
   const float c = A.center ? tile[(r0 + (A.l1 - 1) / 2) * Wt + v0 + (l2 - 1) / 2] : 0.f;
   float acc[PX][NF];
 #pragma unroll
@@ -230,6 +192,81 @@ __global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A) {
       else
         static_cast<uint16_t*>(A.out)[m * plane + (int64_t)u * A.ow + v] = (uint16_t)code;
     }
+  }
+}
+
+
+// Persistent, double-buffered: each block stages its filters once, then walks
+// tiles (map, band of output rows) with the next tile's input rows in flight
+// (cp.async, zero-filled padding) while the current one is computed.
+template <int NF, int PX, int L2, int MODE>
+__global__ void __launch_bounds__(CONV_THREADS) conv_s1_kernel(ConvArgs A, int max_rows) {
+  extern __shared__ __align__(16) float smf[];
+  const int l2 = L2 > 0 ? L2 : A.l2;
+  const int d = A.l1 * l2;
+  const int Wt = conv_tile_width(A.ow, l2, PX);
+  float* wsm = smf;                                // [d][NF] zero-mean taps when centering
+  float* bufs = wsm + d * NF;                      // 2 x [max_rows][Wt]
+  const int buf_elems = max_rows * Wt;
+  const int G = (A.ow + PX - 1) / PX;              // thread groups per output row
+  const int64_t per_map = (int64_t)A.oh * G;
+  const int blocks_per_map = (int)((per_map + CONV_THREADS - 1) / CONV_THREADS);
+  const int64_t total = A.n_maps * blocks_per_map;
+  __shared__ float wmean[NF];
+  if (threadIdx.x < NF) {
+    double s = 0.0;
+    if (A.center && (int)threadIdx.x < A.count)
+      for (int k = 0; k < d; ++k) s += (double)A.pack[k * A.count + threadIdx.x];
+    wmean[threadIdx.x] = (float)(s / d);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < d * NF; e += blockDim.x) {
+    const int k = e / NF, g = e % NF;
+    wsm[e] = g < A.count ? (float)((double)A.pack[k * A.count + g] - (double)wmean[g]) : 0.f;
+  }
+  auto band = [&](int64_t t, int& u_first, int& rows, int64_t& m, int64_t& i0) {
+    m = t / blocks_per_map;
+    i0 = (t % blocks_per_map) * (int64_t)CONV_THREADS;
+    u_first = (int)(i0 / G);
+    const int u_last = (int)((min(per_map, i0 + CONV_THREADS) - 1) / G);
+    rows = u_last - u_first + A.l1;
+  };
+  auto issue = [&](int64_t t, float* buf) {
+    int u_first, rows;
+    int64_t m, i0;
+    band(t, u_first, rows, m, i0);
+    const float* img = A.in + m * (int64_t)A.p * A.q;
+    for (int r = threadIdx.x >> 5; r < rows; r += CONV_THREADS / 32) {
+      const int i = u_first + r - A.top;
+      const bool rok = i >= 0 && i < A.p;
+      for (int c = threadIdx.x & 31; c < Wt; c += 32) {
+        const int j = c - A.left;
+        const bool ok = rok && j >= 0 && j < A.q;
+        cp_async4z(buf + r * Wt + c, ok ? img + (int64_t)i * A.q + j : A.in, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  int64_t t = blockIdx.x;
+  if (t < total) issue(t, bufs);
+  for (int it = 0; t < total; t += gridDim.x, ++it) {
+    float* cur = bufs + (it & 1) * buf_elems;
+    if (t + gridDim.x < total)
+      issue(t + gridDim.x, bufs + ((it + 1) & 1) * buf_elems);
+    else
+      asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    int u_first, rows;
+    int64_t m, i0;
+    band(t, u_first, rows, m, i0);
+    const int64_t item = i0 + threadIdx.x;
+    if (item < per_map) {
+      const int u = (int)(item / G);
+      const int v0 = (int)(item % G) * PX;
+      conv_strip<NF, PX, L2, MODE>(A, wsm, cur, Wt, m, u, v0, u - u_first);
+    }
+    __syncthreads();
   }
 }
 
@@ -390,22 +427,28 @@ static int launch_s1(const ConvArgs& A, cudaStream_t st) {
   const int64_t per_map = (int64_t)A.oh * G;
   const int bpm = (int)((per_map + CONV_THREADS - 1) / CONV_THREADS);
   const int max_rows = (CONV_THREADS + G - 1) / G + 1 + A.l1;
-  const size_t smem = sizeof(float) * ((size_t)A.l1 * l2 * NF + (size_t)max_rows * conv_tile_width(A.ow, l2, PX));
-  const int64_t nblocks = (int64_t)bpm * A.n_maps;
-  if (nblocks > 0x7fffffffLL) return fail(DDCCA_ECONFIG, "conv: too many maps in one call");
+  const size_t smem =
+      sizeof(float) * ((size_t)A.l1 * l2 * NF + 2 * (size_t)max_rows * conv_tile_width(A.ow, l2, PX));
+  const int64_t tiles = (int64_t)bpm * A.n_maps;
   if (smem > 200 * 1024) return fail(DDCCA_ECONFIG, "conv: map row too wide for shared-memory staging");
-#define DDCCA_CONV_L2(N)                                                                                   \
-  case N:                                                                                                  \
-    cudaFuncSetAttribute(conv_s1_kernel<NF, PX, N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    conv_s1_kernel<NF, PX, N, MODE><<<(unsigned)nblocks, CONV_THREADS, smem, st>>>(A);                   \
-    break;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CONV_THREADS, smem);
+    const int64_t grid = std::min<int64_t>(tiles, (int64_t)std::max(1, per_sm) * sms);
+    kern<<<(unsigned)grid, CONV_THREADS, smem, st>>>(A, max_rows);
+  };
   switch (l2) {
-    DDCCA_CONV_L2(3) DDCCA_CONV_L2(5) DDCCA_CONV_L2(7) DDCCA_CONV_L2(9)
-    default:
-      cudaFuncSetAttribute(conv_s1_kernel<NF, PX, 0, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      conv_s1_kernel<NF, PX, 0, MODE><<<(unsigned)nblocks, CONV_THREADS, smem, st>>>(A);
+    case 3: go(conv_s1_kernel<NF, PX, 3, MODE>); break;
+    case 5: go(conv_s1_kernel<NF, PX, 5, MODE>); break;
+    case 7: go(conv_s1_kernel<NF, PX, 7, MODE>); break;
+    case 9: go(conv_s1_kernel<NF, PX, 9, MODE>); break;
+    default: go(conv_s1_kernel<NF, PX, 0, MODE>);
   }
-#undef DDCCA_CONV_L2
   return check_launch("conv_s1_kernel");
 }
 

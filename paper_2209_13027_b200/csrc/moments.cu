@@ -40,7 +40,7 @@ namespace ddcca {
 
 constexpr int KDX = 3;       // dx lags per thread
 constexpr int TILE_X = 32;   // first-pixel columns per block (one per lane)
-constexpr int STAGE_ROWS = 48;  // staged rows per cp.async stage (all maps of the stage)
+constexpr int STAGE_ROWS = 72;  // staged rows per cp.async stage (all maps of the stage)
 constexpr int MAPS_PER_SPLIT = 128;
 constexpr int MAX_LAG_L = 12;  // lag path for windows up to 12 x 12
 
@@ -107,25 +107,28 @@ static void make_plan(const Geo& g, Plan* P) {
   P->NDX = P->G * KDX;
   P->NDF = g.l1 * P->NDX;
   // one stage stages at most PF_ROWS rows per warp: slab + halo must fit
-  P->slab = g.l1 * std::max(1, 32 / g.l1);  // whole ring turns
+  P->slab = g.l1 * std::max(1, 63 / g.l1);  // whole ring turns
   P->tasks.clear();
   P->recs.clear();
   P->lane_slot.clear();
   int nrec = 0;
-  int y = 0;
-  while (y < g.Hp) {
+  // First pixels outside the image are zero padding: their products vanish, so
+  // tasks cover only image rows [top, top+p) and image columns [left, left+q).
+  const int yimg_end = g.top + g.p, ximg_end = g.left + g.q;
+  int y = g.top;
+  while (y < yimg_end) {
     int rz = P->z.rz_of_y[y];
     int y_end = y;
-    while (y_end < g.Hp && P->z.rz_of_y[y_end] == rz) ++y_end;
+    while (y_end < yimg_end && P->z.rz_of_y[y_end] == rz) ++y_end;
     for (int ys = y; ys < y_end; ys += P->slab) {
       int ye = std::min(y_end, ys + P->slab);
-      for (int x0 = 0; x0 < g.Wp; x0 += TILE_X) {
+      for (int x0 = g.left; x0 < ximg_end; x0 += TILE_X) {
         Task t;
         t.y0 = ys; t.y1 = ye; t.x0 = x0; t.rz = rz; t.rec0 = nrec; t.nrec = 0;
         bool has_big = false;
         for (int l = 0; l < TILE_X; ++l) {
           int x = x0 + l;
-          if (x < g.Wp && P->z.cz_of_x[x] == P->z.big_cz) has_big = true;
+          if (x < ximg_end && P->z.cz_of_x[x] == P->z.big_cz) has_big = true;
         }
         if (has_big) {
           P->recs.push_back({rz, P->z.big_cz});
@@ -133,7 +136,7 @@ static void make_plan(const Geo& g, Plan* P) {
         }
         for (int l = 0; l < TILE_X; ++l) {
           int x = x0 + l;
-          if (x < g.Wp && P->z.cz_of_x[x] != P->z.big_cz) {
+          if (x < ximg_end && P->z.cz_of_x[x] != P->z.big_cz) {
             P->lane_slot.push_back(t.nrec);
             P->recs.push_back({rz, P->z.cz_of_x[x]});
             t.nrec++;
@@ -163,7 +166,7 @@ struct LagArgs {
   const int* lane_slot;     // [task][32]
   const int64_t* batch_off; // device copy of batch map offsets
   double* rec;              // [batch][view][split][nrec][NDF]
-  int p, q, top, left, Wp, l2, G, NDX, NDF, nrec, nsplit, nbatch;
+  int p, q, top, left, Wp, l2, G, NDX, NDF, nrec, nsplit, nbatch, xend;
 };
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   // lanes outside the map's padded width hold zeros already (tile zero-filled)
   const int slot = A.lane_slot[task * TILE_X + lane];
   const int x = T.x0 + lane;
-  const bool in_big = (slot < 0) && (x < A.Wp);
+  const bool in_big = (slot < 0) && (x < A.xend);
   double* out = A.rec + (((int64_t)batch * 2 + view) * A.nsplit + split) * (int64_t)A.nrec * A.NDF;
   const int any_big = __any_sync(0xffffffffu, in_big);
 #pragma unroll
@@ -852,6 +855,7 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     A.rec = reinterpret_cast<double*>(w + L.off_rec);
     A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
     A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.nbatch = n_batches;
+    A.xend = g.left + g.q;
     // float64 compute tile + two float32 cp.async buffers
     const size_t smem = (sizeof(double) + 2 * sizeof(float)) * max_stage * (TILE_X + P.NDX - 1);
     dim3 grid((unsigned)P.tasks.size(), (unsigned)L.nsplit, (unsigned)(n_batches * 2));

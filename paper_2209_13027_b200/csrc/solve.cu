@@ -16,7 +16,7 @@
 
 namespace ddcca {
 
-constexpr int SOLVE_THREADS = 512;
+constexpr int SOLVE_THREADS = 256;
 constexpr int SMEM_JACOBI_MAX_N = 110;  // 2*n*n doubles in shared memory
 
 struct Blk {
@@ -115,17 +115,18 @@ __device__ __forceinline__ int lex_cmp(const double* v, int n, int ld, int i, in
   return 0;
 }
 
-// Symmetric eigensolver (solver.py:90-158). s: input n x n (global). Results:
-// w (n), v (n x n row-major, column j = eigenvector j). a, tmp: n*n scratch
-// (shared or global). Returns DDCCA_* status (uniform across the block).
-__device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double* a, double* tmp, double* wtmp,
-                           Blk& B) {
+// Symmetric eigensolver (solver.py:90-158). s: input n x n. Results: w (n),
+// v (n x n row-major, column j = eigenvector j). The rotation working set
+// (a, the accumulated rotations va, and the per-round (c, s) table cs) lives in
+// shared memory; tmp / wtmp are global scratch for the final ordering.
+// Returns a DDCCA_* status (uniform across the block).
+__device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double* a, double* va, double* cs,
+                           double* tmp, double* wtmp, Blk& B) {
   const int nn = n * n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double mx = 0.0;
   for (int e = threadIdx.x; e < nn; e += blockDim.x) mx = fmax(mx, fabs(s[e]));
   mx = block_max(mx, B);
-  // identity start
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) v[e] = (e / n == e % n) ? 1.0 : 0.0;
   if (n == 1 || mx == 0.0) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) wtmp[i] = s[i * n + i];
     __syncthreads();
@@ -153,13 +154,13 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
   for (int e = threadIdx.x; e < nn; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
     a[e] = 0.5 * (s[e] / mx + s[j * n + i] / mx) * f;
+    va[e] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   const int m = n + (n & 1);
   const int npair = m / 2;
-  double* cs = wtmp;            // reuse: c in [0, npair), s in [npair, 2*npair) -> needs 2*npair <= n+1
-  int* pp = B.iscr;             // p of pair t
-  int* qq = B.iscr + npair;     // q of pair t (or -1 if inactive/dummy)
+  int* pp = B.iscr;          // p of pair t
+  int* qq = B.iscr + npair;  // q of pair t (or -1 if inactive / dummy)
   bool converged = false;
   for (int sweep = 0; sweep < 100; ++sweep) {
     if (offdiag_norm(a, n, B) <= 1e-12) { converged = true; break; }
@@ -188,31 +189,33 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
         cs[2 * t + 1] = sn;
       }
       __syncthreads();
-      // rows: B = J^T a
-      for (int e = threadIdx.x; e < npair * n; e += blockDim.x) {
-        const int t = e / n, j = e - t * n;
+      // rows: B = J^T a   (warp per pair, lanes over columns)
+      for (int t = warp; t < npair; t += nwarps) {
         const int q = qq[t];
         if (q < 0) continue;
         const int p = pp[t];
         const double c = cs[2 * t], sn = cs[2 * t + 1];
-        const double ap = a[p * n + j], aq = a[q * n + j];
-        a[p * n + j] = c * ap - sn * aq;
-        a[q * n + j] = sn * ap + c * aq;
+        for (int j = lane; j < n; j += 32) {
+          const double ap = a[p * n + j], aq = a[q * n + j];
+          a[p * n + j] = c * ap - sn * aq;
+          a[q * n + j] = sn * ap + c * aq;
+        }
       }
       __syncthreads();
-      // columns: a = B J, v = v J
-      for (int e = threadIdx.x; e < npair * n; e += blockDim.x) {
-        const int t = e / n, i = e - t * n;
+      // columns: a = B J, va = va J
+      for (int t = warp; t < npair; t += nwarps) {
         const int q = qq[t];
         if (q < 0) continue;
         const int p = pp[t];
         const double c = cs[2 * t], sn = cs[2 * t + 1];
-        const double bp = a[i * n + p], bq = a[i * n + q];
-        a[i * n + p] = c * bp - sn * bq;
-        a[i * n + q] = sn * bp + c * bq;
-        const double vp = v[i * n + p], vq = v[i * n + q];
-        v[i * n + p] = c * vp - sn * vq;
-        v[i * n + q] = sn * vp + c * vq;
+        for (int i = lane; i < n; i += 32) {
+          const double bp = a[i * n + p], bq = a[i * n + q];
+          a[i * n + p] = c * bp - sn * bq;
+          a[i * n + q] = sn * bp + c * bq;
+          const double vp = va[i * n + p], vq = va[i * n + q];
+          va[i * n + p] = c * vp - sn * vq;
+          va[i * n + q] = sn * vp + c * vq;
+        }
       }
       __syncthreads();
     }
@@ -234,7 +237,7 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int r = desc_rank(wtmp, n, i);
     w[r] = wtmp[i];
-    for (int k = 0; k < n; ++k) tmp[k * n + r] = v[k * n + i];
+    for (int k = 0; k < n; ++k) tmp[k * n + r] = va[k * n + i];
   }
   __syncthreads();
   // sign rule
@@ -292,9 +295,9 @@ __device__ void matmul(const double* A, bool ta, const double* Bm, bool tb, doub
 }
 
 // inv_sqrt (solver.py:161-170) into r; eigen scratch from the caller.
-__device__ int inv_sqrt_dev(const double* c, int n, double* r, double* w, double* v, double* a, double* tmp,
-                            double* wtmp, Blk& B) {
-  int rc = sym_eig_dev(c, n, w, v, a, tmp, wtmp, B);
+__device__ int inv_sqrt_dev(const double* c, int n, double* r, double* w, double* v, double* a, double* va, double* cs,
+                            double* tmp, double* wtmp, Blk& B) {
+  int rc = sym_eig_dev(c, n, w, v, a, va, cs, tmp, wtmp, B);
   if (rc != DDCCA_OK) return rc;
   if (!(w[n - 1] > 0.0)) return DDCCA_ENUMERICAL;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
@@ -378,17 +381,19 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
   const int n = S.d, C = S.C, L = S.count;
   const int nn = n * n;
   int* iscr = reinterpret_cast<int*>(sm);  // 2n+2 ints
-  double* base = sm + (2 * n + 2 + 1) / 2 + 1;
-  double *ja, *jtmp;
+  double* cs = sm + (2 * n + 2 + 1) / 2 + 1;  // 2n+2 doubles: per-round rotations
+  double* base = cs + 2 * n + 2;
+  double *ja, *jva;
   double* g = S.ws;
   if (S.jacobi_in_smem) {
     ja = base;
-    jtmp = base + nn;
+    jva = base + nn;
   } else {
     ja = g;
-    jtmp = g + nn;
+    jva = g + nn;
     g += 2 * nn;
   }
+  double* jtmp = g; g += nn;
   Blk B{red, &flag, iscr};
   double* c11 = S.fin;
   double* c22 = S.fin + nn;
@@ -414,8 +419,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
     return;
   }
   // ---- whitening (solver.py:227-229)
-  int rc = inv_sqrt_dev(c11, n, R1, lam, ev, ja, jtmp, wsc, B);
-  if (rc == DDCCA_OK) rc = inv_sqrt_dev(c22, n, R2, lam, ev, ja, jtmp, wsc, B);
+  int rc = inv_sqrt_dev(c11, n, R1, lam, ev, ja, jva, cs, jtmp, wsc, B);
+  if (rc == DDCCA_OK) rc = inv_sqrt_dev(c22, n, R2, lam, ev, ja, jva, cs, jtmp, wsc, B);
   if (rc != DDCCA_OK) {
     if (threadIdx.x == 0) *S.status = rc;
     return;
@@ -432,7 +437,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
     }
   }
   __syncthreads();
-  rc = sym_eig_dev(ev, n, lam, U, ja, jtmp, wsc, B);
+  rc = sym_eig_dev(ev, n, lam, U, ja, jva, cs, jtmp, wsc, B);
   if (rc != DDCCA_OK) {
     if (threadIdx.x == 0) *S.status = rc;
     return;
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
       }
     }
     __syncthreads();
-    rc = sym_eig_dev(ev, n, lam2, NB, ja, jtmp, wsc, B);
+    rc = sym_eig_dev(ev, n, lam2, NB, ja, jva, cs, jtmp, wsc, B);
     if (rc != DDCCA_OK) {
       if (threadIdx.x == 0) *S.status = rc;
       return;
@@ -544,25 +549,27 @@ __global__ void __launch_bounds__(SOLVE_THREADS) sym_eig_kernel(EigArgs E) {
   __shared__ int flag;
   const int n = E.n, nn = n * n;
   int* iscr = reinterpret_cast<int*>(sm);
-  double* base = sm + (2 * n + 2 + 1) / 2 + 1;
+  double* cs = sm + (2 * n + 2 + 1) / 2 + 1;
+  double* base = cs + 2 * n + 2;
   double* g = E.ws;
-  double *ja, *jtmp;
+  double *ja, *jva;
   if (E.jacobi_in_smem) {
     ja = base;
-    jtmp = base + nn;
+    jva = base + nn;
   } else {
     ja = g;
-    jtmp = g + nn;
+    jva = g + nn;
     g += 2 * nn;
   }
+  double* jtmp = g; g += nn;
   double* vv = g; g += nn;
   double* wsc = g; g += 2 * n + 2;
   Blk B{red, &flag, iscr};
   int rc;
   if (E.mode == 0) {
-    rc = sym_eig_dev(E.s, n, E.w, E.v, ja, jtmp, wsc, B);
+    rc = sym_eig_dev(E.s, n, E.w, E.v, ja, jva, cs, jtmp, wsc, B);
   } else {
-    rc = inv_sqrt_dev(E.s, n, E.v, E.w, vv, ja, jtmp, wsc, B);
+    rc = inv_sqrt_dev(E.s, n, E.v, E.w, vv, ja, jva, cs, jtmp, wsc, B);
   }
   if (threadIdx.x == 0) *E.status = rc;
 }
@@ -572,7 +579,7 @@ __global__ void pack_kernel(const double* f, int n, float* out) {
 }
 
 static size_t jacobi_smem(int n, bool in_smem) {
-  size_t ints = sizeof(double) * ((2 * n + 2 + 1) / 2 + 1);
+  size_t ints = sizeof(double) * ((2 * n + 2 + 1) / 2 + 1 + 2 * n + 2);
   return ints + (in_smem ? sizeof(double) * 2 * (size_t)n * n : 0);
 }
 
@@ -584,7 +591,7 @@ extern "C" {
 
 size_t ddcca_solve_workspace(int dim) {
   const size_t nn = (size_t)dim * dim;
-  return sizeof(double) * (12 * nn + 8 * (size_t)dim + 16);
+  return sizeof(double) * (14 * nn + 8 * (size_t)dim + 16);
 }
 
 int ddcca_solve(const double* payload, int dim, int class_count, double epsilon, int count, double* fin, double* w1,
