@@ -40,7 +40,7 @@ namespace ddcca {
 
 constexpr int KDX = 3;       // dx lags per thread
 constexpr int TILE_X = 32;   // first-pixel columns per block (one per lane)
-constexpr int STAGE_ROWS = 72;  // staged rows per cp.async stage (all maps of the stage)
+constexpr int STAGE_ROWS = 48;  // staged rows per cp.async stage (all maps of the stage)
 constexpr int MAPS_PER_SPLIT = 128;
 constexpr int MAX_LAG_L = 12;  // lag path for windows up to 12 x 12
 
@@ -107,7 +107,7 @@ static void make_plan(const Geo& g, Plan* P) {
   P->NDX = P->G * KDX;
   P->NDF = g.l1 * P->NDX;
   // one stage stages at most PF_ROWS rows per warp: slab + halo must fit
-  P->slab = g.l1 * std::max(1, 63 / g.l1);  // whole ring turns
+  P->slab = g.l1 * std::max(1, (STAGE_ROWS - g.l1 + 1) / g.l1);  // whole ring turns that fit a stage
   P->tasks.clear();
   P->recs.clear();
   P->lane_slot.clear();
@@ -169,21 +169,15 @@ struct LagArgs {
   int p, q, top, left, Wp, l2, G, NDX, NDF, nrec, nsplit, nbatch, xend;
 };
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = valid ? 4 : 0;  // src-size 0 => zero fill
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-
 // Sum over rows [0, nrows) of one staged map tile (float64, row stride tc) of
 // own * partner for the L1 x KDX lags of this thread. Rows are processed in
 // whole ring turns of L1; rows >= nrows are masked through the own value
-// (their staged data is still valid partner data for earlier rows).
-template <int L1, bool SKIP0>
-__device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int tc, int nrows, int cown, int cpart,
-                                               double (&acc)[L1][KDX]) {
+// (their staged data is still valid partner data for earlier rows). TC > 0
+// makes the tile stride a compile-time constant (all smem offsets immediate).
+template <int L1, int TC, bool SKIP0>
+__device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int tc_rt, int nrows, int cown,
+                                               int cpart, double (&acc)[L1][KDX]) {
+  const int tc = TC > 0 ? TC : tc_rt;
   double ring[L1][KDX];
   const double* pp = t + cpart;
 #pragma unroll
@@ -195,27 +189,26 @@ __device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int
   for (int r0 = 0; r0 < nrows; r0 += L1) {
 #pragma unroll
     for (int u = 0; u < L1; ++u) {
-      constexpr int dummy = 0;
-      (void)dummy;
       const int snew = (u + L1 - 1) % L1;
 #pragma unroll
-      for (int k = 0; k < KDX; ++k) ring[snew][k] = pp[k];
-      pp += tc;
-      double own = *po;
-      po += tc;
+      for (int k = 0; k < KDX; ++k) ring[snew][k] = pp[u * tc + k];
+      double own = po[u * tc];
       own = (r0 + u < nrows) ? own : 0.0;
 #pragma unroll
       for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy)
 #pragma unroll
         for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, ring[(u + dy) % L1][k], acc[dy][k]);
     }
+    pp += L1 * tc;
+    po += L1 * tc;
   }
 }
 
 // Tasks shorter than one ring turn (the single border rows): direct partner loads.
-template <int L1>
-__device__ __forceinline__ void lag_accumulate_short(const double* __restrict__ t, int tc, int nrows, int cown,
+template <int L1, int TC>
+__device__ __forceinline__ void lag_accumulate_short(const double* __restrict__ t, int tc_rt, int nrows, int cown,
                                                      int cpart, bool skip0, double (&acc)[L1][KDX]) {
+  const int tc = TC > 0 ? TC : tc_rt;
   for (int r = 0; r < nrows; ++r) {
     const double own = t[r * tc + cown];
     const double* pp = t + r * tc + cpart;
@@ -228,7 +221,18 @@ __device__ __forceinline__ void lag_accumulate_short(const double* __restrict__ 
   }
 }
 
-template <int L1>
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 4 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+
+// One block = one task (row range x 32-column tile) of one (batch, view, split);
+// it walks the split's maps in stages of mb maps. Staging: cp.async float32 copies
+// into a per-thread-owned raw buffer (double buffered), each thread converts its
+// own elements to float64 into the (double-buffered) compute tile, then a single
+// __syncthreads per stage publishes it.
+template <int L1, int TC>
 __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArgs A) {
   extern __shared__ __align__(16) double smem_d[];
   const int task = blockIdx.x;
@@ -242,13 +246,14 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   const int nrows = T.y1 - T.y0;
   const bool short_task = nrows < L1;
   const int nrows_pad = short_task ? nrows : (nrows + L1 - 1) / L1 * L1;
-  const int tr = nrows_pad + L1 - 1;              // staged rows per map (zero beyond the map)
-  const int tc = TILE_X + A.NDX - 1;              // staged cols: [x0-(l2-1), x0-(l2-1)+tc), tc <= 64
+  const int tr = nrows_pad + L1 - 1;                   // staged rows per map (zero beyond the map)
+  const int tc = TC > 0 ? TC : TILE_X + A.NDX - 1;     // staged cols: [x0-(l2-1), x0-(l2-1)+tc), tc <= 64
   const int tile_elems = tr * tc;
   const int mb = T.mb;
-  const int stage_elems = mb * tile_elems;
-  double* f64 = smem_d;                                             // [mb][tr][tc] float64
-  float* raw = reinterpret_cast<float*>(smem_d + stage_elems);      // 2 x [mb][tr][tc] float32
+  const int stage_rows = mb * tr;
+  const int stage_elems = stage_rows * tc;
+  double* f64 = smem_d;                                                  // 2 x [mb][tr][tc] float64
+  float* raw = reinterpret_cast<float*>(smem_d + 2 * stage_elems);       // 2 x [mb][tr][tc] float32
   const int xs = T.x0 - (A.l2 - 1);
   const int64_t m_begin = A.batch_off[batch];
   const int64_t m_end = A.batch_off[batch + 1];
@@ -257,26 +262,33 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   const int64_t mbnd = min(m_end, ma + per);
   const float* src = view == 0 ? A.maps[0] : A.maps[1];
   const int64_t plane = (int64_t)A.p * A.q;
+  // this thread's two staging columns
+  const int c0 = lane, c1 = lane + 32;
+  const int col0 = xs + c0 - A.left, col1 = xs + c1 - A.left;
+  const bool cok0 = col0 >= 0 && col0 < A.q;
+  const bool cok1 = c1 < tc && col1 >= 0 && col1 < A.q;
+  const bool has1 = c1 < tc;
 
-  // cp.async staging: warp w copies flat rows fr = w, w + nwarps, ... (fr = j * tr + r),
-  // lanes copy tile columns lane and lane + 32; out-of-image elements are zero-filled.
+  // staged flat rows fr = j * tr + r owned by warp fr % nwarps (no division: (j, r) advance incrementally)
   auto issue = [&](int64_t ms, float* dst) {
-    for (int fr = grp; fr < mb * tr; fr += nwarps) {
-      const int j = fr / tr, r = fr - j * tr;
+    int j = 0, r = grp;
+    while (r >= tr) { r -= tr; ++j; }
+    for (int fr = grp; fr < stage_rows; fr += nwarps) {
       const int img_row = T.y0 + r - A.top;
       const bool rok = img_row >= 0 && img_row < A.p && (r < nrows + L1 - 1) && (ms + j < mbnd);
       const float* rowp = src + (ms + j) * plane + (int64_t)img_row * A.q;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = lane + 32 * h;
-        if (c < tc) {
-          const int col = xs + c - A.left;
-          const bool ok = rok && col >= 0 && col < A.q;
-          cp_async4(dst + fr * tc + c, ok ? rowp + col : src, ok);
-        }
-      }
+      cp_async4(dst + fr * tc + c0, (rok && cok0) ? rowp + col0 : src, rok && cok0);
+      if (has1) cp_async4(dst + fr * tc + c1, (rok && cok1) ? rowp + col1 : src, rok && cok1);
+      r += nwarps;
+      while (r >= tr) { r -= tr; ++j; }
     }
-    cp_async_commit();
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  auto convert = [&](const float* from, double* to) {
+    for (int fr = grp; fr < stage_rows; fr += nwarps) {
+      to[fr * tc + c0] = (double)from[fr * tc + c0];
+      if (has1) to[fr * tc + c1] = (double)from[fr * tc + c1];
+    }
   };
 
   double acc[L1][KDX];
@@ -293,26 +305,25 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   if (ma < mbnd) issue(ma, raw);
   int s = 0;
   for (int64_t ms = ma; ms < mbnd; ms += mb, ++s) {
-    float* cur = raw + (s & 1) * stage_elems;
     if (ms + mb < mbnd)
       issue(ms + mb, raw + ((s + 1) & 1) * stage_elems);
     else
-      cp_async_commit();  // keep one group per iteration for wait_group 1
-    cp_async_wait1();
-    __syncthreads();  // stage s visible to all; previous compute on f64 finished
-    for (int e = threadIdx.x; e < stage_elems; e += blockDim.x) f64[e] = (double)cur[e];
+      asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    double* tile = f64 + (s & 1) * stage_elems;
+    convert(raw + (s & 1) * stage_elems, tile);  // own elements only: no barrier needed before
     __syncthreads();
     const int nm = (int)min((int64_t)mb, mbnd - ms);
     for (int j = 0; j < nm; ++j) {
+      const double* t = tile + j * tile_elems;
       if (short_task)
-        lag_accumulate_short<L1>(f64 + j * tile_elems, tc, nrows, cown, cpart, skip0, acc);
+        lag_accumulate_short<L1, TC>(t, tc, nrows, cown, cpart, skip0, acc);
       else if (skip0)
-        lag_accumulate<L1, true>(f64 + j * tile_elems, tc, nrows, cown, cpart, acc);
+        lag_accumulate<L1, TC, true>(t, tc, nrows, cown, cpart, acc);
       else
-        lag_accumulate<L1, false>(f64 + j * tile_elems, tc, nrows, cown, cpart, acc);
+        lag_accumulate<L1, TC, false>(t, tc, nrows, cown, cpart, acc);
     }
   }
-  // lanes outside the map's padded width hold zeros already (tile zero-filled)
   const int slot = A.lane_slot[task * TILE_X + lane];
   const int x = T.x0 + lane;
   const bool in_big = (slot < 0) && (x < A.xend);
@@ -856,16 +867,24 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
     A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.nbatch = n_batches;
     A.xend = g.left + g.q;
-    // float64 compute tile + two float32 cp.async buffers
-    const size_t smem = (sizeof(double) + 2 * sizeof(float)) * max_stage * (TILE_X + P.NDX - 1);
+    // two float64 compute tiles + two float32 cp.async buffers
+    const size_t smem = (2 * sizeof(double) + 2 * sizeof(float)) * max_stage * (TILE_X + P.NDX - 1);
     dim3 grid((unsigned)P.tasks.size(), (unsigned)L.nsplit, (unsigned)(n_batches * 2));
     dim3 block(32 * P.G);
-    switch (g.l1) {
-#define DDCCA_LAG_CASE(N)                                                                          \
-  case N:                                                                                          \
-    cudaFuncSetAttribute(lag_zone_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    cudaFuncSetAttribute(lag_zone_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);    \
-    lag_zone_kernel<N><<<grid, block, smem, st>>>(A);                                              \
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      kern<<<grid, block, smem, st>>>(A);
+    };
+    const int tcv = TILE_X + P.NDX - 1;
+    if (g.l1 == 3 && tcv == 37) go(lag_zone_kernel<3, 37>);
+    else if (g.l1 == 5 && tcv == 40) go(lag_zone_kernel<5, 40>);
+    else if (g.l1 == 7 && tcv == 46) go(lag_zone_kernel<7, 46>);
+    else if (g.l1 == 9 && tcv == 49) go(lag_zone_kernel<9, 49>);
+    else switch (g.l1) {
+#define DDCCA_LAG_CASE(N) \
+  case N:                 \
+    go(lag_zone_kernel<N, 0>); \
     break;
       DDCCA_LAG_CASE(1) DDCCA_LAG_CASE(2) DDCCA_LAG_CASE(3) DDCCA_LAG_CASE(4) DDCCA_LAG_CASE(5)
       DDCCA_LAG_CASE(6) DDCCA_LAG_CASE(7) DDCCA_LAG_CASE(8) DDCCA_LAG_CASE(9) DDCCA_LAG_CASE(10)
