@@ -53,8 +53,10 @@ int main() {
   double *out, *src;
   cudaMalloc(&out, 8192); cudaMalloc(&src, 8192); cudaMemset(src, 0, 8192);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  int blocks = 148 * 4, threads = 256, iters = 2048;
-  for (int rep = 0; rep < 2; ++rep) {
+  int threads = 128, iters = 2048;
+  for (int per = 1; per <= 8; per *= 2) {
+    int blocks = 148 * per;
+    printf("warps/SM = %d\n", per * 4);
     float ms;
     cudaEventRecord(e0); dfma_ring<<<blocks, threads>>>(out, src, iters); cudaEventRecord(e1); cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1); printf("ring pattern: %.1f TFLOP/s\n", 2.0 * 21 * iters * (double)blocks * threads / ms / 1e9);
