@@ -220,6 +220,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         step()
     ex.synchronize()
     prof.clear()
+    eng.work.clear()
     eng.launches = 0
     barrier()
     torch.cuda.synchronize()
@@ -247,8 +248,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     kern = {}
     for name, evs in prof.items():
         times = [a.elapsed_time(b) for a, b in evs]
+        w = dict(eng.work.get(name) or {})
+        if w.get("calls"):
+            # per-launch algorithmic work = total over the timed steps / launches
+            for key in ("flops", "bytes"):
+                w[key] = w[key] / w["calls"]
         kern[name] = {"ms_avg": sum(times) / len(times), "launches": len(times),
-                      "ms_per_step": sum(times) / args.steps, "work": getattr(eng, "work", {}).get(name)}
+                      "ms_per_step": sum(times) / args.steps, "work": w or None}
 
     # e2e through the public API with host buffers
     e2e = None

@@ -50,6 +50,8 @@ _SIGNATURES = {
     "ddcca_iq_expand": (_i32, [_vp, _i32, _i64, _i32, _i32, _vp, _vp, _vp]),
     "ddcca_im2col": (_i32, [_vp, _i64, _GP, _i32, _vp, _vp]),
     "ddcca_sign_hash": (_i32, [_vp, _i64, _i32, _i64, _vp, _vp]),
+    "ddcca_conv_hw": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _vp, _vp]),
+    "ddcca_conv_hist_hw": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -1,0 +1,375 @@
+// K6 / K6-final+K7+K8 with filter taps in the constant bank.
+//
+// Same arithmetic as conv.cu (zero-mean taps, per-thread DC shift c, float32
+// FFMA, filter-minor output; sign-hash LSB-first; block histograms), but the
+// taps travel as a kernel parameter block, so every FFMA reads its weight
+// straight from the constant bank (FFMA R, R, c[0x0][imm], R): no weight
+// loads, no register-bank pressure from a third register operand, and the
+// whole (L1 x L2 x NF) tap loop is unrolled with immediate offsets.
+//
+// conv_hist_kernel fuses the last layer: a CTA owns BR block-rows of one map
+// (BR * bh output rows x nbx * bw columns, the only pixels the histograms
+// read), computes the sign codes of that band into shared memory and builds
+// the per-block histograms with warp-private shared bins, writing the counts
+// straight into the feature matrix. Codes never reach HBM.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ddcca {
+
+constexpr int CC_THREADS = 256;
+
+template <int N>
+struct Taps {
+  float w[N];
+};
+
+struct CArgs {
+  const float* in;
+  int64_t n_maps;
+  int p, q, top, left, oh, ow, count, center;
+  void* out;
+  // fused histogram
+  int bh, bw, nby, nbx, br, kind, nbits;
+  void* counts;
+  int64_t gpr, row_stride, group_stride;
+};
+
+__device__ __forceinline__ void cp_async4c(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0));
+}
+
+__host__ __device__ inline int cc_tile_width(int cols, int l2, int px) {
+  const int G = (cols + px - 1) / px;
+  return ((G * px + l2 + 3) + 3) / 4 * 4;
+}
+
+// PX x NF responses of the strip starting at tile row r0, column v0.
+template <int L1, int L2, int NF, int PX>
+__device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const float* __restrict__ tile, int Wt, int r0,
+                                         int v0, bool center, float (&acc)[PX][NF]) {
+  const float c = center ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + (L2 - 1) / 2] : 0.f;
+#pragma unroll
+  for (int j = 0; j < PX; ++j)
+#pragma unroll
+    for (int g = 0; g < NF; ++g) acc[j][g] = 0.f;
+#pragma unroll
+  for (int a = 0; a < L1; ++a) {
+    const float* row = tile + (r0 + a) * Wt + v0;
+    constexpr int NX = PX + L2 - 1;
+    float x[(NX + 3) / 4 * 4];
+#pragma unroll
+    for (int t4 = 0; t4 < (NX + 3) / 4; ++t4) {
+      const float4 v = *reinterpret_cast<const float4*>(row + 4 * t4);
+      x[4 * t4 + 0] = v.x - c;
+      x[4 * t4 + 1] = v.y - c;
+      x[4 * t4 + 2] = v.z - c;
+      x[4 * t4 + 3] = v.w - c;
+    }
+#pragma unroll
+    for (int b = 0; b < L2; ++b)
+#pragma unroll
+      for (int g = 0; g < NF; ++g)
+#pragma unroll
+        for (int j = 0; j < PX; ++j) acc[j][g] = fmaf(T.w[(a * L2 + b) * NF + g], x[j + b], acc[j][g]);
+  }
+}
+
+template <int NF, int PX>
+__device__ __forceinline__ unsigned cc_code(const float (&acc)[PX][NF], int j, int count) {
+  unsigned code = 0;
+#pragma unroll
+  for (int g = 0; g < NF; ++g)
+    if (g < count && acc[j][g] > 0.f) code |= 1u << g;
+  return code;
+}
+
+// Stage rows [row0, row0 + rows) (padded coordinates) x tile columns [0, Wt) of map m.
+__device__ __forceinline__ void cc_issue(const CArgs& A, int64_t m, int row0, int rows, int Wt, float* buf) {
+  const float* img = A.in + m * (int64_t)A.p * A.q;
+  for (int r = threadIdx.x >> 5; r < rows; r += CC_THREADS / 32) {
+    const int i = row0 + r - A.top;
+    const bool rok = i >= 0 && i < A.p;
+    const float* rowp = img + (int64_t)i * A.q;
+    for (int c = threadIdx.x & 31; c < Wt; c += 32) {
+      const int j = c - A.left;
+      const bool ok = rok && j >= 0 && j < A.q;
+      cp_async4c(buf + r * Wt + c, ok ? rowp + j : A.in, ok);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// Persistent float-response conv (MODE 0): tiles = (map, band of rows_per_tile output rows).
+template <int L1, int L2, int NF, int PX>
+__global__ void __launch_bounds__(CC_THREADS) conv_c_kernel(CArgs A, Taps<L1 * L2 * NF> T) {
+  extern __shared__ __align__(16) float sm[];
+  const int G = (A.ow + PX - 1) / PX;
+  const int Wt = cc_tile_width(A.ow, L2, PX);
+  const int rows_out = max(1, CC_THREADS / G);  // output rows per tile (one strip per thread)
+  const int rows_in = rows_out + L1 - 1;
+  const int bands = (A.oh + rows_out - 1) / rows_out;
+  const int64_t total = A.n_maps * bands;
+  float* bufs = sm;
+  const int belems = rows_in * Wt;
+  int64_t t = blockIdx.x;
+  if (t < total) cc_issue(A, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
+  const int64_t plane = (int64_t)A.oh * A.ow;
+  for (int it = 0; t < total; t += gridDim.x, ++it) {
+    const float* cur = bufs + (it & 1) * belems;
+    const int64_t tn = t + gridDim.x;
+    if (tn < total)
+      cc_issue(A, tn / bands, (int)(tn % bands) * rows_out, rows_in, Wt, bufs + ((it + 1) & 1) * belems);
+    else
+      asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    const int64_t m = t / bands;
+    const int u0 = (int)(t % bands) * rows_out;
+    const int r = threadIdx.x / G, gi = threadIdx.x % G;
+    const int u = u0 + r;
+    if (r < rows_out && u < A.oh) {
+      const int v0 = gi * PX;
+      float acc[PX][NF];
+      cc_strip<L1, L2, NF, PX>(T, cur, Wt, r, v0, A.center, acc);
+      float* o = static_cast<float*>(A.out) + m * A.count * plane + (int64_t)u * A.ow + v0;
+      if (v0 + PX <= A.ow && (A.ow & 3) == 0 && PX % 4 == 0) {
+#pragma unroll
+        for (int g = 0; g < NF; ++g)
+          if (g < A.count)
+#pragma unroll
+            for (int j4 = 0; j4 < PX / 4; ++j4)
+              *reinterpret_cast<float4*>(o + g * plane + 4 * j4) =
+                  make_float4(acc[4 * j4][g], acc[4 * j4 + 1][g], acc[4 * j4 + 2][g], acc[4 * j4 + 3][g]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < PX; ++j)
+          if (v0 + j < A.ow)
+#pragma unroll
+            for (int g = 0; g < NF; ++g)
+              if (g < A.count) o[g * plane + j] = acc[j][g];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Fused last layer: codes of BR block-rows in shared memory -> block histograms -> counts.
+template <int L1, int L2, int NF, int PX>
+__global__ void __launch_bounds__(CC_THREADS) conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T) {
+  extern __shared__ __align__(16) float sm[];
+  const int cols = A.nbx * A.bw;                 // only pixels inside blocks are needed
+  const int G = (cols + PX - 1) / PX;
+  const int Wt = cc_tile_width(cols, L2, PX);
+  const int rows_out = A.br * A.bh;
+  const int rows_in = rows_out + L1 - 1;
+  const int belems = rows_in * Wt;
+  const int bands = (A.nby + A.br - 1) / A.br;
+  const int64_t total = A.n_maps * bands;
+  const int nbins = 1 << A.nbits;
+  const int words = (nbins + 1) / 2;
+  const int nwarps = CC_THREADS / 32;
+  float* bufs = sm;                                               // 2 x [rows_in][Wt]
+  uint16_t* codes = reinterpret_cast<uint16_t*>(bufs + 2 * belems);  // [rows_out][cols]
+  unsigned* bins = reinterpret_cast<unsigned*>(codes + ((rows_out * cols + 1) & ~1));  // [nwarps][words]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t t = blockIdx.x;
+  if (t < total) cc_issue(A, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
+  for (int it = 0; t < total; t += gridDim.x, ++it) {
+    const float* cur = bufs + (it & 1) * belems;
+    const int64_t tn = t + gridDim.x;
+    if (tn < total)
+      cc_issue(A, tn / bands, (int)(tn % bands) * rows_out, rows_in, Wt, bufs + ((it + 1) & 1) * belems);
+    else
+      asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    const int64_t m = t / bands;
+    const int by0 = (int)(t % bands) * A.br;
+    const int nbr = min(A.br, A.nby - by0);      // block rows in this band
+    // 1) codes of the band into shared memory
+    for (int s = threadIdx.x; s < nbr * A.bh * G; s += CC_THREADS) {
+      const int r = s / G, v0 = (s % G) * PX;
+      float acc[PX][NF];
+      cc_strip<L1, L2, NF, PX>(T, cur, Wt, r, v0, A.center, acc);
+#pragma unroll
+      for (int j = 0; j < PX; ++j)
+        if (v0 + j < cols) codes[r * cols + v0 + j] = (uint16_t)cc_code<NF, PX>(acc, j, A.count);
+    }
+    __syncthreads();
+    // 2) one warp per block: warp-private bins, counts out
+    unsigned* wb = bins + warp * words;
+    for (int blk = warp; blk < nbr * A.nbx; blk += nwarps) {
+      const int rb = blk / A.nbx, bx = blk % A.nbx;
+      for (int w = lane; w < words; w += 32) wb[w] = 0u;
+      __syncwarp();
+      for (int px = lane; px < A.bh * A.bw; px += 32) {
+        const int r = rb * A.bh + px / A.bw, c = bx * A.bw + px % A.bw;
+        const unsigned code = codes[r * cols + c];
+        atomicAdd(&wb[code >> 1], 1u << ((code & 1u) * 16));
+      }
+      __syncwarp();
+      const int64_t blk_global = (int64_t)(by0 + rb) * A.nbx + bx;
+      const int64_t base = (m / A.gpr) * A.row_stride + (m % A.gpr) * A.group_stride + blk_global * nbins;
+      if (A.kind == 2) {
+        uint16_t* o = static_cast<uint16_t*>(A.counts) + base;
+        for (int b = lane; b < nbins; b += 32) o[b] = (uint16_t)((wb[b >> 1] >> ((b & 1) * 16)) & 0xffffu);
+      } else if ((nbins & 7) == 0) {
+        // 8 bins per lane per store
+        uint8_t* o = static_cast<uint8_t*>(A.counts) + base;
+        for (int b8 = lane * 8; b8 < nbins; b8 += 256) {
+          uint32_t lo = 0, hi = 0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            unsigned c = (wb[(b8 + k) >> 1] >> (((b8 + k) & 1) * 16)) & 0xffffu;
+            c = c > 255u ? 255u : c;
+            if (k < 4) lo |= c << (8 * k);
+            else hi |= c << (8 * (k - 4));
+          }
+          *reinterpret_cast<uint2*>(o + b8) = make_uint2(lo, hi);
+        }
+      } else {
+        uint8_t* o = static_cast<uint8_t*>(A.counts) + base;
+        for (int b = lane; b < nbins; b += 32) {
+          const unsigned c = (wb[b >> 1] >> ((b & 1) * 16)) & 0xffffu;
+          o[b] = (uint8_t)(c > 255u ? 255u : c);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------------------------------- host side
+
+static void zero_mean_taps(const float* pack_host, int count, int d, int nf, bool center, float* out) {
+  for (int g = 0; g < nf; ++g) {
+    double mean = 0.0;
+    if (center && g < count) {
+      for (int k = 0; k < d; ++k) mean += (double)pack_host[k * count + g];
+      mean /= d;
+    }
+    for (int k = 0; k < d; ++k)
+      out[k * nf + g] = g < count ? (float)((double)pack_host[k * count + g] - mean) : 0.f;
+  }
+}
+
+// Grid for a persistent kernel: resident CTAs per SM x SMs, capped by the tile count.
+template <typename K>
+static int persistent_grid(K kern, size_t smem, int64_t tiles) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CC_THREADS, smem);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(1, per_sm) * sms));
+  return (int)grid;
+}
+
+template <int L1, int L2, int NF, int PX>
+static int run_conv_c(const CArgs& A, const float* pack_host, cudaStream_t st) {
+  Taps<L1 * L2 * NF> T;
+  zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
+  const int G = (A.ow + PX - 1) / PX;
+  const int Wt = cc_tile_width(A.ow, L2, PX);
+  const int rows_out = std::max(1, CC_THREADS / G);
+  const int rows_in = rows_out + L1 - 1;
+  const size_t smem = sizeof(float) * 2 * (size_t)rows_in * Wt;
+  if (smem > 200 * 1024) return fail(DDCCA_ECONFIG, "conv: map row too wide for shared-memory staging");
+  const int64_t tiles = A.n_maps * ((A.oh + rows_out - 1) / rows_out);
+  auto kern = conv_c_kernel<L1, L2, NF, PX>;
+  const int grid = persistent_grid(kern, smem, tiles);
+  kern<<<grid, CC_THREADS, smem, st>>>(A, T);
+  return check_launch("conv_c_kernel");
+}
+
+template <int L1, int L2, int NF, int PX>
+static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
+  Taps<L1 * L2 * NF> T;
+  zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
+  const int cols = A.nbx * A.bw;
+  const int G = (cols + PX - 1) / PX;
+  // block rows per CTA: about one strip per thread, at least one block row
+  A.br = std::max(1, std::min(A.nby, CC_THREADS / std::max(1, A.bh * G)));
+  const int rows_out = A.br * A.bh;
+  const int Wt = cc_tile_width(cols, L2, PX);
+  const int rows_in = rows_out + L1 - 1;
+  const int nbins = 1 << A.nbits;
+  const size_t smem = sizeof(float) * 2 * (size_t)rows_in * Wt + sizeof(uint16_t) * (((size_t)rows_out * cols + 1) & ~1ull) +
+                      sizeof(unsigned) * (CC_THREADS / 32) * (size_t)((nbins + 1) / 2);
+  if (smem > 220 * 1024) return fail(DDCCA_ECONFIG, "conv_hist: band does not fit shared memory");
+  const int64_t tiles = A.n_maps * ((A.nby + A.br - 1) / A.br);
+  auto kern = conv_hist_kernel<L1, L2, NF, PX>;
+  const int grid = persistent_grid(kern, smem, tiles);
+  kern<<<grid, CC_THREADS, smem, st>>>(A, T);
+  return check_launch("conv_hist_kernel");
+}
+
+// Dispatch over the compiled (window, filter-count) shapes; DDCCA_ECONFIG = not covered.
+template <bool HIST>
+static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cudaStream_t st) {
+#define DDCCA_CC(L, NFV, PXV)                                                                                \
+  if (l1 == L && l2 == L && A.count <= NFV)                                                                  \
+    return HIST ? run_conv_hist<L, L, NFV, PXV>(A, pack_host, st) : run_conv_c<L, L, NFV, PXV>(A, pack_host, st);
+  DDCCA_CC(3, 8, 8)
+  DDCCA_CC(5, 8, 8)
+  DDCCA_CC(7, 8, 8)
+  DDCCA_CC(9, 8, 8)
+  DDCCA_CC(3, 16, 4)
+  DDCCA_CC(5, 16, 4)
+  DDCCA_CC(7, 12, 4)
+  DDCCA_CC(7, 16, 4)
+  DDCCA_CC(9, 12, 4)
+  DDCCA_CC(9, 16, 4)
+#undef DDCCA_CC
+  return fail(DDCCA_ECONFIG, "no constant-bank conv instance for %dx%d with %d filters", l1, l2, A.count);
+}
+
+}  // namespace ddcca
+
+using namespace ddcca;
+
+extern "C" {
+
+int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
+                  int center, float* out, void* stream) {
+  Geo g;
+  DDCCA_TRY(make_geo(gg, &g));
+  if (g.stride != 1) return fail(DDCCA_ECONFIG, "constant-bank conv needs stride 1");
+  if (count < 1 || count > g.d) return fail(DDCCA_ECONFIG, "filter count %d outside [1, %d]", count, g.d);
+  if (!conv_pack_host) return fail(DDCCA_ESHAPE, "null host taps");
+  if (n_maps == 0) return DDCCA_OK;
+  CArgs A{};
+  A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
+  A.count = count; A.center = center; A.out = out;
+  return dispatch<false>(A, g.l1, g.l2, conv_pack_host, as_stream(stream));
+}
+
+int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
+                       int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,
+                       int64_t row_stride, int64_t group_stride, void* stream) {
+  Geo g;
+  DDCCA_TRY(make_geo(gg, &g));
+  if (g.stride != 1) return fail(DDCCA_ECONFIG, "fused conv-histogram needs stride 1");
+  if (count < 1 || count > 16) return fail(DDCCA_ECONFIG, "hash width %d outside the fused path (1..16)", count);
+  if (block_h < 1 || block_w < 1 || g.oh < block_h || g.ow < block_w)
+    return fail(DDCCA_ESHAPE, "%dx%d blocks do not fit a %dx%d map", block_h, block_w, g.oh, g.ow);
+  const int bpc = block_h * block_w;
+  if ((count_kind == 0 && bpc > 255) || (count_kind == 1 && bpc > 510) || bpc > 65535)
+    return fail(DDCCA_ECONFIG, "count storage cannot hold %d pixels per block", bpc);
+  if (!conv_pack_host) return fail(DDCCA_ESHAPE, "null host taps");
+  if (n_maps == 0) return DDCCA_OK;
+  CArgs A{};
+  A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
+  A.count = count; A.center = center; A.out = nullptr;
+  A.bh = block_h; A.bw = block_w; A.nby = g.oh / block_h; A.nbx = g.ow / block_w; A.kind = count_kind;
+  A.nbits = count; A.counts = counts; A.gpr = groups_per_row; A.row_stride = row_stride; A.group_stride = group_stride;
+  return dispatch<true>(A, g.l1, g.l2, conv_pack_host, as_stream(stream));
+}
+
+}  // extern "C"

@@ -53,9 +53,14 @@ class DeviceLayer:
     pack1: object  # torch float32 (d * count) tap-major
     pack2: object
     fin: object = None  # torch float64 (5, d, d): c11, c22, cw, cb, ctilde
+    host1: object = None  # numpy float32 copies of the packs (constant-bank kernels)
+    host2: object = None
 
     def pack(self, view: int):
         return self.pack1 if view == 1 else self.pack2
+
+    def host_pack(self, view: int):
+        return self.host1 if view == 1 else self.host2
 
 
 # ----------------------------------------------------------------------------
@@ -125,7 +130,14 @@ def solve_layer(ex, payload, geom: PatchGeometry, count: int, center: bool, clas
     layer._status = status
     if check:
         check_layer(layer)
+        fetch_host_packs(layer)
     return layer
+
+
+def fetch_host_packs(layer: DeviceLayer) -> None:
+    """Host copies of the float32 taps (tiny) for the constant-bank conv kernels."""
+    layer.host1 = np.ascontiguousarray(layer.pack1.cpu().numpy())
+    layer.host2 = np.ascontiguousarray(layer.pack2.cpu().numpy())
 
 
 def check_layer(layer: DeviceLayer) -> None:
@@ -151,7 +163,10 @@ def layer_from_filters(ex, filters1, filters2, geom: PatchGeometry, center: bool
         _native.check(lib.ddcca_pack_filters(_native.ptr(w), count, geom.dim, _native.ptr(pk),
                                              _native.stream_ptr(ex.stream)), "pack_filters")
         packs.append(pk)
-    return DeviceLayer(geom, bool(center), count, w1, w2, None, packs[0], packs[1])
+    lay = DeviceLayer(geom, bool(center), count, w1, w2, None, packs[0], packs[1])
+    lay.host1 = np.ascontiguousarray(f1.reshape(count, -1).T.astype(np.float32))
+    lay.host2 = np.ascontiguousarray(f2.reshape(count, -1).T.astype(np.float32))
+    return lay
 
 
 def conv(ex, maps, layer: DeviceLayer, view: int, out=None):
@@ -163,9 +178,35 @@ def conv(ex, maps, layer: DeviceLayer, view: int, out=None):
     if out is None:
         out = torch.empty((n, layer.count, oh, ow), dtype=torch.float32, device=ex.device)
     g = layer.geom.native(p, q)
+    hp = layer.host_pack(view)
+    if hp is not None:
+        rc = lib.ddcca_conv_hw(_native.ptr(maps), n, C.byref(g), hp.ctypes.data_as(C.c_void_p), layer.count,
+                               int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream))
+        if rc == _native.OK:
+            return out
+        if rc != _native.ECONFIG:
+            _native.check(rc, "conv")
     _native.check(lib.ddcca_conv(_native.ptr(maps), n, C.byref(g), _native.ptr(layer.pack(view)), layer.count,
                                  int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream)), "conv")
     return out
+
+
+def conv_hist(ex, maps, layer: DeviceLayer, view: int, plan, counts_base, kind: int, groups_per_row: int,
+              row_stride: int, group_stride: int) -> bool:
+    """Fused last-layer conv + sign hash + block histograms; False if the shape is not covered."""
+    lib = _native.load()
+    hp = layer.host_pack(view)
+    if hp is None or plan.sh != plan.bh or plan.sw != plan.bw:
+        return False
+    n, p, q = maps.shape
+    g = layer.geom.native(p, q)
+    rc = lib.ddcca_conv_hist_hw(_native.ptr(maps), n, C.byref(g), hp.ctypes.data_as(C.c_void_p), layer.count,
+                                int(layer.center), plan.bh, plan.bw, _native.ptr(counts_base), kind, groups_per_row,
+                                row_stride, group_stride, _native.stream_ptr(ex.stream))
+    if rc == _native.ECONFIG:
+        return False
+    _native.check(rc, "conv_hist")
+    return True
 
 
 def conv_hash(ex, maps, layer: DeviceLayer, view: int, out=None):
@@ -272,8 +313,11 @@ class Engine:
 
     def _timed(self, name: str, kernels: int, work: dict | None, fn, *a, **k):
         self.launches += kernels
-        if work is not None:
-            self.work[name] = work
+        if work is not None and self.profile is not None:
+            acc = self.work.setdefault(name, {"kind": work.get("kind"), "flops": 0.0, "bytes": 0.0, "calls": 0})
+            acc["flops"] += work.get("flops", 0.0)
+            acc["bytes"] += work.get("bytes", 0.0)
+            acc["calls"] += 1
         if self.profile is None:
             return fn(*a, **k)
         torch = _torch()
@@ -442,9 +486,15 @@ class Engine:
                     oh, ow = last.geom.out_shape(pp, qq)
                     fl = 2.0 * n * oh * ow * last.count * last.geom.dim
                     by = 4.0 * n * pp * qq + n * oh * ow * (1 if last.count <= 8 else 2)
+                    base = out[s0:s1].view(-1)[(view - 1) * per_view:]
+                    nb_cols = plan.nbx * plan.bw
+                    fl_f = 2.0 * n * plan.nby * plan.bh * nb_cols * last.count * last.geom.dim
+                    by_f = 4.0 * n * pp * qq + n * plan.blocks * plan.bins * out.element_size()
+                    if self._timed("conv_hist", 1, {"kind": "fma", "flops": fl_f, "bytes": by_f}, conv_hist, ex, maps,
+                                   last, view, plan, base, kind, groups, featlen, plan.blocks * plan.bins):
+                        continue
                     codes = self._timed("conv_hash", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv_hash, ex,
                                         maps, last, view)
-                    base = out[s0:s1].view(-1)[(view - 1) * per_view:]
                     hb = codes.numel() * codes.element_size() + n * plan.blocks * plan.bins * out.element_size()
                     self._timed("block_hist", 1, {"kind": "hbm", "bytes": float(hb)}, lambda: _native.check(
                         lib.ddcca_block_hist(

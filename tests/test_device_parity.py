@@ -294,3 +294,48 @@ def test_fit_transform_end_to_end_vs_oracle(ex):
     got = P.compute_features(ds, bank, cfg, ex)
     want = O.features(v1, v2, _oracle_layers(bank), O.EncodeCfg(7, 7), batch=32)
     assert np.mean(got == want) >= 0.999
+
+
+# ------------------------------------------------------------------------ constant-bank / fused kernels
+
+@pytest.mark.parametrize("l,count,p,q", [(7, 8, 40, 36), (5, 8, 23, 30), (9, 12, 33, 41), (3, 8, 17, 19),
+                                         (7, 16, 24, 29), (9, 8, 30, 30)])
+def test_constant_bank_conv_matches_oracle(ex, l, count, p, q):
+    rng = np.random.default_rng(l * 31 + count)
+    stack = rng.uniform(size=(5, p, q)).astype(np.float32)
+    f = rng.standard_normal((count, l, l))
+    geom = P.PatchGeometry(l, l)
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, geom, True)
+        assert lay.host1 is not None
+        got = E.conv(ex, torch.from_numpy(stack).to(ex.device), lay, 1).cpu().numpy()
+    ref = O.conv_stack(stack, O.Layer(f, f, O.Geometry(l, l), True), 1)
+    scale = np.abs(f).sum(axis=(1, 2)).max()
+    assert np.abs(got - ref).max() <= 3e-6 * scale
+
+
+@pytest.mark.parametrize("l,count,p,q,bh,bw", [(7, 8, 64, 48, 16, 16), (5, 8, 28, 23, 7, 7), (9, 12, 40, 40, 8, 8),
+                                               (3, 4, 17, 19, 4, 5), (7, 8, 33, 65, 16, 16), (5, 6, 20, 20, 20, 20)])
+def test_fused_conv_hist_matches_oracle(ex, l, count, p, q, bh, bw):
+    rng = np.random.default_rng(l + count + bh)
+    n_in, b = 3, 4
+    maps = rng.standard_normal((b * n_in, p, q)).astype(np.float32)
+    f = rng.standard_normal((count, l, l))
+    geom = P.PatchGeometry(l, l)
+    enc = P.EncoderConfig(bh, bw)
+    plan = E.block_plan(enc, p, q, count)
+    kind = E.count_kind(plan.bpc)
+    featlen = n_in * plan.blocks * plan.bins
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, geom, True)
+        out = torch.zeros((b, featlen), dtype=torch.int16 if kind == 2 else torch.uint8, device=ex.device)
+        ok = E.conv_hist(ex, torch.from_numpy(maps).to(ex.device), lay, 1, plan, out.view(-1), kind, n_in, featlen,
+                         plan.blocks * plan.bins)
+        assert ok
+        got = E.decode_counts(out.cpu().numpy(), plan)
+    resp = O.conv_stack(maps, O.Layer(f, f, O.Geometry(l, l), True), 1)  # (b*n_in, count, p, q)
+    want = np.stack([np.concatenate([O.block_counts(O.combine_bits(O.sign_bits(resp[i * n_in + g])),
+                                                    O.EncodeCfg(bh, bw), count).reshape(-1) for g in range(n_in)])
+                     for i in range(b)])
+    assert got.shape == want.shape
+    assert np.mean(got == want) >= 0.999
