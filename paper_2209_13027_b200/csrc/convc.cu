@@ -56,7 +56,9 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
   for (int j = 0; j < PX; ++j)
 #pragma unroll
     for (int g = 0; g < NF; ++g) acc[j][g] = 0.f;
-#pragma unroll
+  // rows stay rolled (keeps the loop body inside the instruction cache); taps of a
+  // row are warp-uniform constant-bank loads feeding the FFMAs
+#pragma unroll 1
   for (int a = 0; a < L1; ++a) {
     const float* row = tile + (r0 + a) * Wt + v0;
     constexpr int NX = PX + L2 - 1;
