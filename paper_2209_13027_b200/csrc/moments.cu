@@ -40,6 +40,7 @@ namespace ddcca {
 
 constexpr int KDX = 3;       // dx lags per thread
 constexpr int TILE_X = 32;   // first-pixel columns per block (one per lane)
+constexpr bool LAG_F32 = true;  // float32 tiles, convert in the ring (halves shared-memory traffic)
 constexpr int STAGE_ROWS = 48;  // staged rows per cp.async stage (all maps of the stage)
 constexpr int MAPS_PER_SPLIT = 128;
 constexpr int MAX_LAG_L = 12;  // lag path for windows up to 12 x 12
@@ -174,25 +175,25 @@ struct LagArgs {
 // whole ring turns of L1; rows >= nrows are masked through the own value
 // (their staged data is still valid partner data for earlier rows). TC > 0
 // makes the tile stride a compile-time constant (all smem offsets immediate).
-template <int L1, int TC, bool SKIP0>
-__device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int tc_rt, int nrows, int cown,
+template <int L1, int TC, bool SKIP0, typename S>
+__device__ __forceinline__ void lag_accumulate(const S* __restrict__ t, int tc_rt, int nrows, int cown,
                                                int cpart, double (&acc)[L1][KDX]) {
   const int tc = TC > 0 ? TC : tc_rt;
   double ring[L1][KDX];
-  const double* pp = t + cpart;
+  const S* pp = t + cpart;
 #pragma unroll
   for (int q = 0; q < L1 - 1; ++q)
 #pragma unroll
-    for (int k = 0; k < KDX; ++k) ring[q][k] = pp[q * tc + k];
+    for (int k = 0; k < KDX; ++k) ring[q][k] = (double)pp[q * tc + k];
   pp += (L1 - 1) * tc;
-  const double* po = t + cown;
+  const S* po = t + cown;
   for (int r0 = 0; r0 < nrows; r0 += L1) {
 #pragma unroll
     for (int u = 0; u < L1; ++u) {
       const int snew = (u + L1 - 1) % L1;
 #pragma unroll
-      for (int k = 0; k < KDX; ++k) ring[snew][k] = pp[u * tc + k];
-      double own = po[u * tc];
+      for (int k = 0; k < KDX; ++k) ring[snew][k] = (double)pp[u * tc + k];
+      double own = (double)po[u * tc];
       own = (r0 + u < nrows) ? own : 0.0;
 #pragma unroll
       for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy)
@@ -205,18 +206,18 @@ __device__ __forceinline__ void lag_accumulate(const double* __restrict__ t, int
 }
 
 // Tasks shorter than one ring turn (the single border rows): direct partner loads.
-template <int L1, int TC>
-__device__ __forceinline__ void lag_accumulate_short(const double* __restrict__ t, int tc_rt, int nrows, int cown,
+template <int L1, int TC, typename S>
+__device__ __forceinline__ void lag_accumulate_short(const S* __restrict__ t, int tc_rt, int nrows, int cown,
                                                      int cpart, bool skip0, double (&acc)[L1][KDX]) {
   const int tc = TC > 0 ? TC : tc_rt;
   for (int r = 0; r < nrows; ++r) {
-    const double own = t[r * tc + cown];
-    const double* pp = t + r * tc + cpart;
+    const double own = (double)t[r * tc + cown];
+    const S* pp = t + r * tc + cpart;
 #pragma unroll
     for (int dy = 0; dy < L1; ++dy) {
       if (dy == 0 && skip0) continue;
 #pragma unroll
-      for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, pp[dy * tc + k], acc[dy][k]);
+      for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, (double)pp[dy * tc + k], acc[dy][k]);
     }
   }
 }
@@ -232,7 +233,7 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool val
 // into a per-thread-owned raw buffer (double buffered), each thread converts its
 // own elements to float64 into the (double-buffered) compute tile, then a single
 // __syncthreads per stage publishes it.
-template <int L1, int TC>
+template <int L1, int TC, bool F32>
 __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArgs A) {
   extern __shared__ __align__(16) double smem_d[];
   const int task = blockIdx.x;
@@ -252,8 +253,10 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   const int mb = T.mb;
   const int stage_rows = mb * tr;
   const int stage_elems = stage_rows * tc;
-  double* f64 = smem_d;                                                  // 2 x [mb][tr][tc] float64
-  float* raw = reinterpret_cast<float*>(smem_d + 2 * stage_elems);       // 2 x [mb][tr][tc] float32
+  // F32: three float32 stages, the ring converts on load. Else: two float32 cp.async
+  // stages converted by their owners into two float64 compute tiles.
+  double* f64 = smem_d;                                                                   // 2 x stage (float64)
+  float* raw = F32 ? reinterpret_cast<float*>(smem_d) : reinterpret_cast<float*>(smem_d + 2 * stage_elems);
   const int xs = T.x0 - (A.l2 - 1);
   const int64_t m_begin = A.batch_off[batch];
   const int64_t m_end = A.batch_off[batch + 1];
@@ -302,6 +305,30 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   // groups whose dx are all negative skip the dy = 0 lag (canonical half-plane only)
   const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
 
+  if constexpr (F32) {
+    if (ma < mbnd) issue(ma, raw); else asm volatile("cp.async.commit_group;\n" ::);
+    if (ma + mb < mbnd) issue(ma + mb, raw + stage_elems); else asm volatile("cp.async.commit_group;\n" ::);
+    int s = 0;
+    for (int64_t ms = ma; ms < mbnd; ms += mb, ++s) {
+      asm volatile("cp.async.wait_group 1;\n" ::);
+      __syncthreads();  // stage s visible; everybody finished stage s-1 (its buffer is reused below)
+      if (ms + 2 * mb < mbnd)
+        issue(ms + 2 * mb, raw + ((s + 2) % 3) * stage_elems);
+      else
+        asm volatile("cp.async.commit_group;\n" ::);
+      const float* tile = raw + (s % 3) * stage_elems;
+      const int nm = (int)min((int64_t)mb, mbnd - ms);
+      for (int j = 0; j < nm; ++j) {
+        const float* t = tile + j * tile_elems;
+        if (short_task)
+          lag_accumulate_short<L1, TC>(t, tc, nrows, cown, cpart, skip0, acc);
+        else if (skip0)
+          lag_accumulate<L1, TC, true>(t, tc, nrows, cown, cpart, acc);
+        else
+          lag_accumulate<L1, TC, false>(t, tc, nrows, cown, cpart, acc);
+      }
+    }
+  } else {
   if (ma < mbnd) issue(ma, raw);
   int s = 0;
   for (int64_t ms = ma; ms < mbnd; ms += mb, ++s) {
@@ -323,6 +350,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
       else
         lag_accumulate<L1, TC, false>(t, tc, nrows, cown, cpart, acc);
     }
+  }
   }
   const int slot = A.lane_slot[task * TILE_X + lane];
   const int x = T.x0 + lane;
@@ -867,8 +895,9 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
     A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.nbatch = n_batches;
     A.xend = g.left + g.q;
-    // two float64 compute tiles + two float32 cp.async buffers
-    const size_t smem = (2 * sizeof(double) + 2 * sizeof(float)) * max_stage * (TILE_X + P.NDX - 1);
+    // F32: three float32 stages; else two float64 compute tiles + two float32 cp.async stages
+    const size_t smem = (LAG_F32 ? 3 * sizeof(float) : 2 * sizeof(double) + 2 * sizeof(float)) * max_stage *
+                        (TILE_X + P.NDX - 1);
     dim3 grid((unsigned)P.tasks.size(), (unsigned)L.nsplit, (unsigned)(n_batches * 2));
     dim3 block(32 * P.G);
     auto go = [&](auto kern) {
@@ -877,14 +906,14 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       kern<<<grid, block, smem, st>>>(A);
     };
     const int tcv = TILE_X + P.NDX - 1;
-    if (g.l1 == 3 && tcv == 37) go(lag_zone_kernel<3, 37>);
-    else if (g.l1 == 5 && tcv == 40) go(lag_zone_kernel<5, 40>);
-    else if (g.l1 == 7 && tcv == 46) go(lag_zone_kernel<7, 46>);
-    else if (g.l1 == 9 && tcv == 49) go(lag_zone_kernel<9, 49>);
+    if (g.l1 == 3 && tcv == 37) go(lag_zone_kernel<3, 37, LAG_F32>);
+    else if (g.l1 == 5 && tcv == 40) go(lag_zone_kernel<5, 40, LAG_F32>);
+    else if (g.l1 == 7 && tcv == 46) go(lag_zone_kernel<7, 46, LAG_F32>);
+    else if (g.l1 == 9 && tcv == 49) go(lag_zone_kernel<9, 49, LAG_F32>);
     else switch (g.l1) {
 #define DDCCA_LAG_CASE(N) \
   case N:                 \
-    go(lag_zone_kernel<N, 0>); \
+    go(lag_zone_kernel<N, 0, LAG_F32>); \
     break;
       DDCCA_LAG_CASE(1) DDCCA_LAG_CASE(2) DDCCA_LAG_CASE(3) DDCCA_LAG_CASE(4) DDCCA_LAG_CASE(5)
       DDCCA_LAG_CASE(6) DDCCA_LAG_CASE(7) DDCCA_LAG_CASE(8) DDCCA_LAG_CASE(9) DDCCA_LAG_CASE(10)
