@@ -258,11 +258,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # e2e through the public API with host buffers
     e2e = None
+    eng.maps_cache = None
+    del counts_buf[:]
+    torch.cuda.empty_cache()
     if not args.no_e2e:
         h1 = img1.cpu().pin_memory()
         h2 = img2.cpu().pin_memory()
         hl = torch.from_numpy(lab.astype(np.int64))
-        host_counts = torch.empty(counts_buf[0].shape, dtype=counts_buf[0].dtype).pin_memory()
+        host_counts = torch.empty((s1 - s0, featlen), dtype=torch.int16 if kind == 2 else torch.uint8).pin_memory()
         ds = P.ViewPairDataset.from_arrays(h1.numpy(), h2.numpy(), hl.numpy(), class_count=classes)
         ds._stacks = (h1, h2, hl.numpy())
         net = P.NetworkConfig(tuple(layer_cfgs), batch=P.BatchSpec(bs))
@@ -270,9 +273,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
         def e2e_step():
             bank = P.train_network(ds, net, ex)
-            counts, _ = P.compute_feature_counts(ds, bank, pcfg, ex)
-            with torch.cuda.stream(ex.stream):
-                host_counts.copy_(counts, non_blocking=True)
+            P.compute_feature_counts(ds, bank, pcfg, ex, host_out=host_counts)
+            ds._device_state = None  # next step uploads again (H2D inside the timed region)
             return bank
 
         for _ in range(max(1, min(2, args.warmup))):
@@ -292,7 +294,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         t = torch.tensor([ms_e], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        h2d = 2 * (s1 - s0) * p * q * 4
+        h2d = 2 * (s1 - s0) * p * q * 4 + (s1 - s0) * 8
         d2h = host_counts.numel() * host_counts.element_size()
         e2e = {"value": M / (float(t.item()) / 1000.0), "unit": "images/s", "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "ms_per_step": float(t.item())}

@@ -96,10 +96,15 @@ def _executor(executor):
 
 
 def _to_dev32(ex, a):
+    """Host array (numpy or pinned torch tensor) -> float32 device tensor on the executor's stream."""
     import torch
 
-    t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
-    return t.to(ex.device, non_blocking=True) if t.is_pinned() else t.to(ex.device)
+    if isinstance(a, torch.Tensor):
+        t = a if a.dtype == torch.float32 else a.float()
+        t = t.contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
+    return t.to(ex.device, non_blocking=t.is_pinned())
 
 
 def _labels_dev(ex, labels):
@@ -234,14 +239,23 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
     s1 = gb[mine.stop - 1].stop if len(mine) else 0
     eng = E.Engine(ex)
     with torch.cuda.stream(ex.stream):
-        i1 = _to_dev32(ex, np.asarray(v1)[s0:s1])
-        i2 = _to_dev32(ex, np.asarray(v2)[s0:s1])
+        i1 = _to_dev32(ex, _rows(v1, s0, s1))
+        i2 = _to_dev32(ex, _rows(v2, s0, s1))
         ld = _labels_dev(ex, lab[s0:s1])
         res = eng.fit(i1, i2, ld, ds.class_count, list(cfg.layers), bs, cfg.epsilon, n_global=n, first_sample=s0,
                       stage_hook=stage_hook)
     bank = _bank_from_device(res.layers)
     object.__setattr__(bank, "_device_cache", (str(ex.device), res.layers))
+    # the transform of the same samples reuses the uploaded images and the retained
+    # last-hidden-layer maps (pipeline.compute_feature_counts)
+    ds._device_state = {"device": str(ex.device), "rows": (s0, s1), "images": (i1, i2), "engine": eng,
+                        "bank": id(bank)}
     return bank
+
+
+def _rows(a, s0: int, s1: int):
+    """Row slice of a numpy array or (pinned) torch tensor, without a host copy."""
+    return a[s0:s1]
 
 
 def forward_stacks(view1, view2, bank: FilterBank, executor=None):

@@ -32,6 +32,7 @@ from .errors import ConfigError, ShapeError
 from .patches import PatchGeometry
 
 MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
+KEEP_MAPS_BYTES = 48 << 30  # fit keeps the last layer's input maps (both views) for the transform if they fit
 
 
 def _torch():
@@ -304,9 +305,11 @@ class FitResult:
 class Engine:
     """Fit + transform on device for one executor (one GPU, one sample shard)."""
 
-    def __init__(self, executor, map_budget_bytes: int = MAP_BUDGET_BYTES):
+    def __init__(self, executor, map_budget_bytes: int = MAP_BUDGET_BYTES, keep_maps_bytes: int = KEEP_MAPS_BYTES):
         self.ex = executor
         self.budget = map_budget_bytes
+        self.keep_maps_bytes = keep_maps_bytes
+        self.maps_cache = None  # last hidden layer's maps of the fitted shard, reused by the transform
         self.profile = None   # dict name -> [(start_event, end_event)] when profiling
         self.work = {}        # name -> algorithmic work of one call (for the roofline)
         self.launches = 0     # kernels launched by this engine
@@ -329,17 +332,28 @@ class Engine:
         self.profile.setdefault(name, []).append((s, e))
         return out
 
-    def _forward(self, images, layers: list, view: int):
+    def _forward(self, images, layers: list, view: int, out=None):
+        """Maps after ``layers`` (filter-minor); ``out`` receives the last layer's output."""
         cur = images
         for li, layer in enumerate(layers):
             n, p, q = cur.shape
             oh, ow = layer.geom.out_shape(p, q)
             fl = 2.0 * n * oh * ow * layer.count * layer.geom.dim
             by = 4.0 * n * (p * q + layer.count * oh * ow)
-            out = self._timed(f"conv_l{li + 1}", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv, self.ex, cur,
-                              layer, view)
-            cur = out.view(n * layer.count, oh, ow)
+            dst = out.view(n, layer.count, oh, ow) if (out is not None and li == len(layers) - 1) else None
+            res = self._timed(f"conv_l{li + 1}", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv, self.ex, cur,
+                              layer, view, dst)
+            cur = res.view(n * layer.count, oh, ow)
         return cur
+
+    def _cache_key(self, images1, layers: list):
+        return (images1.data_ptr(), tuple(images1.shape), tuple(id(l) for l in layers))
+
+    def cached_maps(self, images1, layers: list):
+        c = self.maps_cache
+        if c is not None and c["key"] == self._cache_key(images1, layers):
+            return c
+        return None
 
     # -- helpers -------------------------------------------------------------
     def _superbatches(self, batch_ranges: list, bytes_per_sample: int):
@@ -367,20 +381,33 @@ class Engine:
 
     # -- fit -------------------------------------------------------------------
     def layer_partials(self, images1, images2, labels, layers: list, geom: PatchGeometry, center: bool,
-                       classes: int, batch_ranges: list, first_sample: int = 0):
-        """Per-batch partial moments for the given (local) batches; returns (n_batches, plen)."""
+                       classes: int, batch_ranges: list, first_sample: int = 0, keep: bool = False):
+        """Per-batch partial moments for the given (local) batches; returns (n_batches, plen).
+
+        ``keep``: also retain this layer's input maps for the whole shard (when they fit
+        ``keep_maps_bytes``) so the transform does not recompute them.
+        """
         torch = _torch()
         ex = self.ex
-        _, p0, q0 = images1.shape
+        m_local, p0, q0 = images1.shape
         p, q = self._shape_after(p0, q0, layers)
         n_in = self._maps_per_sample(layers)
         plen = payload_len(geom.dim, classes)
         parts = torch.empty((len(batch_ranges), plen), dtype=torch.float64, device=ex.device)
+        keep_buf = None
+        if keep and layers and 2 * m_local * n_in * p * q * 4 <= self.keep_maps_bytes:
+            self.maps_cache = None
+            keep_buf = (torch.empty((m_local * n_in, p, q), dtype=torch.float32, device=ex.device),
+                        torch.empty((m_local * n_in, p, q), dtype=torch.float32, device=ex.device))
         row = 0
         for group in self._superbatches(batch_ranges, n_in * p * q * 4):
             s0, s1 = group[0].start - first_sample, group[-1].stop - first_sample
-            m1 = self._forward(images1[s0:s1], layers, 1)
-            m2 = self._forward(images2[s0:s1], layers, 2)
+            if keep_buf is not None:
+                m1 = self._forward(images1[s0:s1], layers, 1, out=keep_buf[0][s0 * n_in:s1 * n_in])
+                m2 = self._forward(images2[s0:s1], layers, 2, out=keep_buf[1][s0 * n_in:s1 * n_in])
+            else:
+                m1 = self._forward(images1[s0:s1], layers, 1)
+                m2 = self._forward(images2[s0:s1], layers, 2)
             mlab = labels[s0:s1].repeat_interleave(n_in) if n_in > 1 else labels[s0:s1]
             offs = np.cumsum([0] + [len(r) * n_in for r in group], dtype=np.int64)
             nmaps = int(offs[-1])
@@ -391,6 +418,9 @@ class Engine:
                         moments_partials, ex, m1, m2, mlab, offs, geom, center, classes,
                         out=parts[row:row + len(group)])
             row += len(group)
+        if keep_buf is not None:
+            self.maps_cache = {"key": self._cache_key(images1, layers), "m1": keep_buf[0], "m2": keep_buf[1],
+                               "n_in": n_in}
         return parts
 
     def reduce_partials(self, parts, n_global_batches: int, local_batches: range):
@@ -441,8 +471,9 @@ class Engine:
             for i, cfg in enumerate(layer_cfgs):
                 if stage_hook:
                     stage_hook(f"layer {i + 1}: accumulating moments over {len(gb)} batches")
+                last = i == len(layer_cfgs) - 1
                 parts = self.layer_partials(images1, images2, labels, layers, cfg.geom, cfg.center, classes, local,
-                                            first_sample)
+                                            first_sample, keep=last and self.keep_maps_bytes > 0)
                 merged = self.reduce_partials(parts, len(gb), mine)
                 layer = self._timed(f"solve_l{i + 1}", 1, None, solve_layer, ex, merged, cfg.geom, cfg.filters,
                                     cfg.center, classes, eps)
@@ -462,8 +493,12 @@ class Engine:
         featlen = 2 * groups * plan.blocks * plan.bins
         return plan, groups, featlen
 
-    def transform_counts(self, images1, images2, layers: list, enc, batch_size: int, out=None):
-        """(m, p, q) x2 -> per-sample block counts (m, featlen) u8/u16 on device."""
+    def transform_counts(self, images1, images2, layers: list, enc, batch_size: int, out=None, host_out=None):
+        """(m, p, q) x2 -> per-sample block counts (m, featlen) u8/u16 on device.
+
+        ``host_out`` (pinned host tensor of the same shape): each super-batch's counts
+        are copied out on a side stream while the next super-batch is computed.
+        """
         torch = _torch()
         ex = self.ex
         lib = _native.load()
@@ -476,11 +511,17 @@ class Engine:
         ranges = [range(s, min(s + batch_size, m)) for s in range(0, m, batch_size)]
         pm, qm = self._shape_after(p0, q0, layers[:-1])
         per_view = groups * plan.blocks * plan.bins
+        cache = self.cached_maps(images1, layers[:-1])
+        copy_stream = torch.cuda.Stream(device=ex.device) if host_out is not None else None
         with torch.cuda.stream(ex.stream):
             for group in self._superbatches(ranges, groups * pm * qm * 4):
                 s0, s1 = group[0].start, group[-1].stop
                 for view, imgs in ((1, images1), (2, images2)):
-                    maps = self._forward(imgs[s0:s1], layers[:-1], view)
+                    if cache is not None:
+                        src = cache["m1"] if view == 1 else cache["m2"]
+                        maps = src[s0 * groups:s1 * groups]
+                    else:
+                        maps = self._forward(imgs[s0:s1], layers[:-1], view)
                     last = layers[-1]
                     n, pp, qq = maps.shape
                     oh, ow = last.geom.out_shape(pp, qq)
@@ -502,6 +543,14 @@ class Engine:
                             codes.shape[2], plan.n_bits, plan.bh, plan.bw, plan.sh, plan.sw, _native.ptr(base),
                             kind, groups, featlen, plan.blocks * plan.bins, _native.stream_ptr(ex.stream)),
                         "block_hist"))
+                if copy_stream is not None:
+                    ev = torch.cuda.Event()
+                    ev.record(ex.stream)
+                    copy_stream.wait_event(ev)
+                    with torch.cuda.stream(copy_stream):
+                        host_out[s0:s1].copy_(out[s0:s1], non_blocking=True)
+            if copy_stream is not None:
+                ex.stream.wait_stream(copy_stream)
         return out, plan
 
     def expand(self, counts, plan: BlockPlan, enc):

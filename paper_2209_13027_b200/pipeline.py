@@ -49,19 +49,37 @@ def _encoder_and_batch(config):
     return enc, batch
 
 
-def compute_feature_counts(ds, bank, config, executor=None):
-    """Device block counts (M_local, featlen) plus the BlockPlan; samples of this rank only."""
+def compute_feature_counts(ds, bank, config, executor=None, host_out=None):
+    """Device block counts plus the BlockPlan for this rank's samples.
+
+    World size 1: all samples. With a process group, the rank's batch shard
+    (the same contiguous shard train_network used), rows [s0, s1) of the
+    dataset. ``host_out``: optional pinned host tensor; counts are streamed into
+    it super-batch by super-batch while the transform proceeds.
+    """
     import torch
+
+    from .patches import batch_partition
 
     ex = _executor(executor)
     enc, bs = _encoder_and_batch(config)
     v1, v2, _ = ds.stacks_view()
-    eng = E.Engine(ex)
+    n = len(ds)
+    gb = batch_partition(n, config.net.batch) if hasattr(config, "net") else [range(0, n)]
+    mine = ex.shard(len(gb))
+    s0 = gb[mine.start].start if len(mine) else 0
+    s1 = gb[mine.stop - 1].stop if len(mine) else 0
+    st = getattr(ds, "_device_state", None)
     with torch.cuda.stream(ex.stream):
         layers = device_layers(bank, ex)
-        i1 = _to_dev32(ex, v1)
-        i2 = _to_dev32(ex, v2)
-        counts, plan = eng.transform_counts(i1, i2, layers, enc, bs)
+        if st is not None and st["device"] == str(ex.device) and st["rows"] == (s0, s1) and st["bank"] == id(bank):
+            eng = st["engine"]
+            i1, i2 = st["images"]
+        else:
+            eng = E.Engine(ex)
+            i1 = _to_dev32(ex, v1[s0:s1])
+            i2 = _to_dev32(ex, v2[s0:s1])
+        counts, plan = eng.transform_counts(i1, i2, layers, enc, bs, host_out=host_out)
     return counts, plan
 
 
