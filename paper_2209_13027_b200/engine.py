@@ -493,11 +493,15 @@ class Engine:
         featlen = 2 * groups * plan.blocks * plan.bins
         return plan, groups, featlen
 
-    def transform_counts(self, images1, images2, layers: list, enc, batch_size: int, out=None, host_out=None):
+    def transform_counts(self, images1, images2, layers: list, enc, batch_size: int, out=None, host_out=None,
+                         sink=None):
         """(m, p, q) x2 -> per-sample block counts (m, featlen) u8/u16 on device.
 
         ``host_out`` (pinned host tensor of the same shape): each super-batch's counts
         are copied out on a side stream while the next super-batch is computed.
+        ``sink(s0, s1, counts)``: streaming consumer; the device buffer then holds
+        one super-batch only (for outputs larger than HBM, e.g. the 3-stage config)
+        and the returned tensor is that rolling buffer.
         """
         torch = _torch()
         ex = self.ex
@@ -506,16 +510,20 @@ class Engine:
         plan, groups, featlen = self.feature_geometry(p0, q0, layers, enc)
         kind = count_kind(plan.bpc)
         dt = torch.int16 if kind == 2 else torch.uint8
-        if out is None:
-            out = torch.empty((m, featlen), dtype=dt, device=ex.device)
         ranges = [range(s, min(s + batch_size, m)) for s in range(0, m, batch_size)]
         pm, qm = self._shape_after(p0, q0, layers[:-1])
         per_view = groups * plan.blocks * plan.bins
+        per_sample = max(groups * pm * qm * 4, featlen * (2 if kind == 2 else 1) if sink is not None else 0)
+        supers = self._superbatches(ranges, per_sample)
+        if out is None:
+            rows = max(g[-1].stop - g[0].start for g in supers) if sink is not None else m
+            out = torch.empty((rows, featlen), dtype=dt, device=ex.device)
         cache = self.cached_maps(images1, layers[:-1])
         copy_stream = torch.cuda.Stream(device=ex.device) if host_out is not None else None
         with torch.cuda.stream(ex.stream):
-            for group in self._superbatches(ranges, groups * pm * qm * 4):
+            for group in supers:
                 s0, s1 = group[0].start, group[-1].stop
+                o0 = 0 if sink is not None else s0  # row offset inside `out`
                 for view, imgs in ((1, images1), (2, images2)):
                     if cache is not None:
                         src = cache["m1"] if view == 1 else cache["m2"]
@@ -527,7 +535,7 @@ class Engine:
                     oh, ow = last.geom.out_shape(pp, qq)
                     fl = 2.0 * n * oh * ow * last.count * last.geom.dim
                     by = 4.0 * n * pp * qq + n * oh * ow * (1 if last.count <= 8 else 2)
-                    base = out[s0:s1].view(-1)[(view - 1) * per_view:]
+                    base = out[o0:o0 + (s1 - s0)].view(-1)[(view - 1) * per_view:]
                     nb_cols = plan.nbx * plan.bw
                     fl_f = 2.0 * n * plan.nby * plan.bh * nb_cols * last.count * last.geom.dim
                     by_f = 4.0 * n * pp * qq + n * plan.blocks * plan.bins * out.element_size()
@@ -548,7 +556,9 @@ class Engine:
                     ev.record(ex.stream)
                     copy_stream.wait_event(ev)
                     with torch.cuda.stream(copy_stream):
-                        host_out[s0:s1].copy_(out[s0:s1], non_blocking=True)
+                        host_out[s0:s1].copy_(out[o0:o0 + (s1 - s0)], non_blocking=True)
+                if sink is not None:
+                    sink(s0, s1, out[:s1 - s0])
             if copy_stream is not None:
                 ex.stream.wait_stream(copy_stream)
         return out, plan
