@@ -432,17 +432,12 @@ class Engine:
             return self._timed("tree", levels, None, tree_merge, ex, parts)
         dist = torch.distributed
         if ex.deterministic:
-            # gather every rank's per-batch partials, rebuild global batch order, same tree everywhere
-            from .execution import shard_range
+            # every rank's per-batch partials in global batch order, same tree everywhere:
+            # bitwise identical to the single-GPU result for any GPU count
+            from .execution import gather_batch_partials
 
-            counts = [len(shard_range(n_global_batches, r, ex.world_size)) for r in range(ex.world_size)]
-            mx = max(counts)
-            pad = torch.zeros((mx, parts.shape[1]), dtype=parts.dtype, device=ex.device)
-            pad[: parts.shape[0]] = parts
-            bufs = [torch.empty_like(pad) for _ in range(ex.world_size)]
             with torch.cuda.stream(ex.stream):
-                dist.all_gather(bufs, pad, group=ex.group)
-            allp = torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0).contiguous()
+                allp = gather_batch_partials(parts, n_global_batches, ex.world_size, ex.group)
             return tree_merge(ex, allp)
         merged = tree_merge(ex, parts)
         with torch.cuda.stream(ex.stream):

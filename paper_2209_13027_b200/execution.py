@@ -102,3 +102,23 @@ def shard_range(n_batches: int, rank: int, world: int) -> range:
     base, extra = divmod(n_batches, world)
     start = rank * base + min(rank, extra)
     return range(start, start + base + (1 if rank < extra else 0))
+
+
+def gather_batch_partials(parts, n_global_batches: int, world: int, group=None):
+    """All ranks' per-batch payload rows in global batch order (deterministic reduction input).
+
+    ``parts``: (n_local, plen) tensor of this rank's batches (its ``shard_range``).
+    Ranks hold different batch counts, so rows are padded to the largest shard
+    for ``all_gather`` and trimmed afterwards. Works for any torch.distributed
+    backend (NCCL with device tensors, gloo with host tensors).
+    """
+    import torch
+    import torch.distributed as dist
+
+    counts = [len(shard_range(n_global_batches, r, world)) for r in range(world)]
+    mx = max(counts)
+    pad = torch.zeros((mx, parts.shape[1]), dtype=parts.dtype, device=parts.device)
+    pad[: parts.shape[0]] = parts
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0).contiguous()
