@@ -41,7 +41,8 @@ namespace ddcca {
 constexpr int KDX = 3;       // dx lags per thread
 constexpr int TILE_X = 32;   // first-pixel columns per block (one per lane)
 constexpr bool LAG_F32 = true;  // float32 tiles, convert in the ring (halves shared-memory traffic)
-constexpr int STAGE_ROWS = 48;  // staged rows per cp.async stage (all maps of the stage)
+constexpr int STAGE_ROWS = 96;  // staged rows per cp.async stage (all maps of the stage)
+constexpr int SLAB_ROWS = 48;   // staged rows of one interior task (slab + halo)
 constexpr int MAPS_PER_SPLIT = 128;
 constexpr int MAX_LAG_L = 12;  // lag path for windows up to 12 x 12
 
@@ -108,7 +109,7 @@ static void make_plan(const Geo& g, Plan* P) {
   P->NDX = P->G * KDX;
   P->NDF = g.l1 * P->NDX;
   // one stage stages at most PF_ROWS rows per warp: slab + halo must fit
-  P->slab = g.l1 * std::max(1, (STAGE_ROWS - g.l1 + 1) / g.l1);  // whole ring turns that fit a stage
+  P->slab = g.l1 * std::max(1, (SLAB_ROWS - g.l1 + 1) / g.l1);  // whole ring turns
   P->tasks.clear();
   P->recs.clear();
   P->lane_slot.clear();
@@ -466,41 +467,79 @@ struct RectArgs {
   const int* rz_of_y; const int* cz_of_x;
   const int* rz_lo; const int* rz_hi; const int* cz_lo; const int* cz_hi;
   int64_t n_maps;
-  int p, q, top, left, Hp, Wp, nrz, ncz, l1, l2, d, center;
+  int p, q, top, left, Hp, Wp, nrz, ncz, l1, l2, d, center, big_cz;
 };
 
-__global__ void rect_sums_kernel(RectArgs A) {
+// Warp per map. Rows are walked zone by zone; every lane keeps the running sums of
+// its own columns (float4 groups), which at a zone boundary go either to the
+// column's singleton zone (border columns) or into the warp-reduced interior
+// zone. Then R[a][b] = sum of the zone sums covering (a, b), centered.
+constexpr int RS_WARPS = 4;
+constexpr int RS_COLS = 8;  // columns per lane (q <= 256)
+
+__global__ void __launch_bounds__(RS_WARPS * 32) rect_sums_kernel(RectArgs A) {
   extern __shared__ double sm[];
-  double* colz = sm;                            // [nrz][Wp]: per column, sum over each row zone
-  double* Zp = sm + (int64_t)A.nrz * A.Wp;      // [nrz][ncz]
-  double* R = Zp + A.nrz * A.ncz;               // [d]
-  const int64_t m = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int zsz = A.nrz * A.ncz;
+  double* Zp = sm + warp * (zsz + A.d);
+  double* R = Zp + zsz;
+  const int64_t m = (int64_t)blockIdx.x * RS_WARPS + warp;
   const int view = blockIdx.y;
+  if (m >= A.n_maps) return;
   const float* img = (view == 0 ? A.maps[0] : A.maps[1]) + m * (int64_t)A.p * A.q;
-  // thread per padded column; rows walked zone by zone (coalesced across threads)
-  for (int x = threadIdx.x; x < A.Wp; x += blockDim.x) {
-    const int j = x - A.left;
-    const bool cok = j >= 0 && j < A.q;
-    int y = 0;
-    for (int rz = 0; rz < A.nrz; ++rz) {
-      double s = 0.0;
-      for (; y < A.Hp && A.rz_of_y[y] == rz; ++y) {
-        const int i = y - A.top;
-        if (cok && i >= 0 && i < A.p) s += (double)__ldg(img + (int64_t)i * A.q + j);
+  for (int e = lane; e < zsz; e += 32) Zp[e] = 0.0;
+  const bool vec = (A.q & 3) == 0;
+  // lane columns: vec -> 4*lane + 128*g + k ; scalar -> lane + 32*k
+  int col[RS_COLS];
+  int czc[RS_COLS];
+#pragma unroll
+  for (int k = 0; k < RS_COLS; ++k) {
+    col[k] = vec ? (4 * lane + 128 * (k >> 2) + (k & 3)) : (lane + 32 * k);
+    czc[k] = col[k] < A.q ? A.cz_of_x[col[k] + A.left] : -1;
+  }
+  __syncwarp();
+  const int big = A.big_cz;
+  int y = 0;
+  for (int rz = 0; rz < A.nrz; ++rz) {
+    double acc[RS_COLS];
+#pragma unroll
+    for (int k = 0; k < RS_COLS; ++k) acc[k] = 0.0;
+    int ye = y;
+    while (ye < A.Hp && A.rz_of_y[ye] == rz) ++ye;
+    const int i0 = max(y - A.top, 0), i1 = min(ye - A.top, A.p);
+    for (int i = i0; i < i1; ++i) {
+      const float* row = img + (int64_t)i * A.q;
+      if (vec) {
+#pragma unroll
+        for (int g = 0; g < RS_COLS / 4; ++g) {
+          const int c0 = 4 * lane + 128 * g;
+          if (c0 < A.q) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(row + c0));
+            acc[4 * g + 0] += (double)v.x;
+            acc[4 * g + 1] += (double)v.y;
+            acc[4 * g + 2] += (double)v.z;
+            acc[4 * g + 3] += (double)v.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < RS_COLS; ++k)
+          if (col[k] < A.q) acc[k] += (double)__ldg(row + col[k]);
       }
-      colz[rz * A.Wp + x] = s;
     }
+    double s_int = 0.0;
+#pragma unroll
+    for (int k = 0; k < RS_COLS; ++k) {
+      if (czc[k] < 0) continue;
+      if (czc[k] == big) s_int += acc[k];
+      else Zp[rz * A.ncz + czc[k]] = acc[k];  // singleton column zone: this lane's column only
+    }
+    s_int = warp_sum(s_int);
+    if (lane == 0 && big >= 0) Zp[rz * A.ncz + big] = s_int;
+    y = ye;
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < A.nrz * A.ncz; e += blockDim.x) {
-    const int rz = e / A.ncz, cz = e % A.ncz;
-    double s = 0.0;
-    for (int x = 0; x < A.Wp; ++x)
-      if (A.cz_of_x[x] == cz) s += colz[rz * A.Wp + x];
-    Zp[e] = s;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < A.d; k += blockDim.x) {
+  __syncwarp();
+  for (int k = lane; k < A.d; k += 32) {
     const int a = k / A.l2, b = k % A.l2;
     double s = 0.0;
     for (int rz = 0; rz < A.nrz; ++rz) {
@@ -510,16 +549,12 @@ __global__ void rect_sums_kernel(RectArgs A) {
     }
     R[k] = s;
   }
-  __syncthreads();
-  __shared__ double mean;
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < A.d; ++k) t += R[k];
-    mean = t / A.d;
-  }
-  __syncthreads();
+  __syncwarp();
+  double t = 0.0;
+  for (int k = lane; k < A.d; k += 32) t += R[k];
+  const double mean = warp_sum(t) / A.d;
   double* o = A.out + ((int64_t)view * A.n_maps + m) * A.d;
-  for (int k = threadIdx.x; k < A.d; k += blockDim.x) o[k] = A.center ? R[k] - mean : R[k];
+  for (int k = lane; k < A.d; k += 32) o[k] = A.center ? R[k] - mean : R[k];
 }
 
 // ----------------------------------------------------------------------------
@@ -948,11 +983,11 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       R.rz_of_y = rz_of_y; R.cz_of_x = cz_of_x; R.rz_lo = rz_lo; R.rz_hi = rz_hi; R.cz_lo = cz_lo; R.cz_hi = cz_hi;
       R.n_maps = n_maps; R.p = g.p; R.q = g.q; R.top = g.top; R.left = g.left; R.Hp = g.Hp; R.Wp = g.Wp;
       R.nrz = P.nrz; R.ncz = P.ncz; R.l1 = g.l1; R.l2 = g.l2; R.d = g.d; R.center = center;
-      const size_t sm = sizeof(double) * ((size_t)P.nrz * g.Wp + (size_t)P.nrz * P.ncz + g.d);
-      if (sm > 200 * 1024) return fail(DDCCA_ECONFIG, "moments: map too wide for the window-sum kernel");
+      R.big_cz = P.z.big_cz;
+      if (g.q > 32 * RS_COLS) return fail(DDCCA_ECONFIG, "moments: maps wider than %d columns", 32 * RS_COLS);
+      const size_t sm = sizeof(double) * RS_WARPS * ((size_t)P.nrz * P.ncz + g.d);
       cudaFuncSetAttribute(rect_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      const int rthreads = std::min(512, (g.Wp + 31) / 32 * 32);
-      rect_sums_kernel<<<dim3((unsigned)n_maps, 2), rthreads, sm, st>>>(R);
+      rect_sums_kernel<<<dim3((unsigned)((n_maps + RS_WARPS - 1) / RS_WARPS), 2), RS_WARPS * 32, sm, st>>>(R);
       DDCCA_TRY(check_launch("moments: rect_sums"));
       batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(R.out, map_label, A.batch_off, n_maps, g.d,
                                                                  class_count, plen, cols_per_map, partials);
