@@ -31,8 +31,11 @@
 //   rect_sums         per-map window sums (class-sum path), centered.
 //   batch_epilogue    per-batch class sums / global sums / counts.
 //   direct_*          explicit-patch float64 path for stride != 1.
-#include <vector>
+#include <cuda.h>
+
 #include <algorithm>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 
@@ -368,6 +371,188 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
       if (lane == 0 && any_big) out[(int64_t)T.rec0 * A.NDF + lag] = v;
       if (slot >= 0) out[(int64_t)(T.rec0 + slot) * A.NDF + lag] = acc[dy][k];
     }
+}
+
+// ----------------------------------------------------------------------------
+// TMA + mbarrier pipeline variant (maps with q % 4 == 0): one elected producer
+// thread streams whole stages (mb maps x tr rows x TCB columns, zero-filled
+// out of bounds = the zero padding) with a single cp.async.bulk.tensor per
+// stage into an NS-deep ring; consumer warps wait on the stage's "full"
+// mbarrier and release it through its "empty" mbarrier. No __syncthreads and
+// no per-element staging instructions in the steady state.
+// ----------------------------------------------------------------------------
+constexpr int TMA_NS = 3;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
+  unsigned done;
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  while (!mbar_try_wait(b, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(tm), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct TmaBoxes {
+  int rows_int, mb_int;      // interior tasks (nrows >= L1)
+  int rows_short, mb_short;  // short (single border row) tasks
+  int shift;                 // columns the tile starts early so the box origin is 16 B aligned
+};
+
+// One launch per (view, task kind): the single tensor map is used directly from
+// the parameter space (no runtime selection of a tensor-map address).
+template <int L1, int TCB>
+__global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
+    lag_tma_kernel(LagArgs A, TmaBoxes bx, const int* __restrict__ task_ids, int view,
+                   const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) float stage_mem[];
+  const int task = task_ids[blockIdx.x];
+  const int split = blockIdx.y;
+  const int batch = blockIdx.z;
+  const TaskDev T = A.tasks[task];
+  const int lane = threadIdx.x & 31;
+  const int grp = threadIdx.x >> 5;
+  const int nrows = T.y1 - T.y0;
+  const bool short_task = nrows < L1;
+  const int trb = short_task ? bx.rows_short : bx.rows_int;  // staged rows per map (box height)
+  const int mb = short_task ? bx.mb_short : bx.mb_int;
+  const int tile_elems = trb * TCB;
+  const int stage_elems = mb * tile_elems;
+  const int max_stage = max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * TCB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_mem + TMA_NS * max_stage);
+  uint64_t* empty = full + TMA_NS;
+  const int64_t m_begin = A.batch_off[batch];
+  const int64_t m_end = A.batch_off[batch + 1];
+  const int64_t per = (m_end - m_begin + A.nsplit - 1) / A.nsplit;
+  const int64_t ma = m_begin + (int64_t)split * per;
+  const int64_t mbnd = min(m_end, ma + per);
+  const int nstages = ma < mbnd ? (int)((mbnd - ma + mb - 1) / mb) : 0;
+  const int G = A.G;  // consumer warps; warp G is the producer
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TMA_NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], G);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (grp >= G) {
+    // ---------------- producer (whole warp stays converged; lane 0 issues) ----------------
+    // TMA box origins must be 16-byte aligned in the innermost dimension: start the
+    // tile bx.shift columns early (consumers offset their columns by the same shift)
+    const int x = T.x0 - (A.l2 - 1) - A.left - bx.shift;  // image column of tile column 0
+    const int y = T.y0 - A.top;                 // image row of tile row 0
+    const unsigned bytes = (unsigned)stage_elems * 4u;
+    for (int s = 0; s < nstages; ++s) {
+      const int slot = s % TMA_NS;
+      if (s >= TMA_NS) mbar_wait(&empty[slot], (unsigned)((s / TMA_NS - 1) & 1));
+      if (lane == 0) {
+        mbar_expect_tx(&full[slot], bytes);
+        tma_load_3d(stage_mem + slot * max_stage, &tmap, x, y, (int)(ma + (int64_t)s * mb), &full[slot]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- consumers ----------------
+    double acc[L1][KDX];
+#pragma unroll
+    for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+      for (int k = 0; k < KDX; ++k) acc[dy][k] = 0.0;
+    const int cown = lane + (A.l2 - 1) + bx.shift;
+    const int cpart = lane + grp * KDX + bx.shift;
+    const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
+    for (int s = 0; s < nstages; ++s) {
+      const int slot = s % TMA_NS;
+      mbar_wait(&full[slot], (unsigned)((s / TMA_NS) & 1));
+      const float* tile = stage_mem + slot * max_stage;
+      const int64_t ms = ma + (int64_t)s * mb;
+      const int nm = (int)min((int64_t)mb, mbnd - ms);
+      for (int j = 0; j < nm; ++j) {
+        const float* t = tile + j * tile_elems;
+        if (short_task)
+          lag_accumulate_short<L1, TCB>(t, TCB, nrows, cown, cpart, skip0, acc);
+        else if (skip0)
+          lag_accumulate<L1, TCB, true>(t, TCB, nrows, cown, cpart, acc);
+        else
+          lag_accumulate<L1, TCB, false>(t, TCB, nrows, cown, cpart, acc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    const int rslot = A.lane_slot[task * TILE_X + lane];
+    const int xg = T.x0 + lane;
+    const bool in_big = (rslot < 0) && (xg < A.xend);
+    double* out = A.rec + (((int64_t)batch * 2 + view) * A.nsplit + split) * (int64_t)A.nrec * A.NDF;
+    const int any_big = __any_sync(0xffffffffu, in_big);
+#pragma unroll
+    for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+      for (int k = 0; k < KDX; ++k) {
+        const int lag = dy * A.NDX + grp * KDX + k;
+        double v = in_big ? acc[dy][k] : 0.0;
+        v = warp_sum(v);
+        if (lane == 0 && any_big) out[(int64_t)T.rec0 * A.NDF + lag] = v;
+        if (rslot >= 0) out[(int64_t)(T.rec0 + rslot) * A.NDF + lag] = acc[dy][k];
+      }
+  }
+  __syncthreads();  // every warp (incl. the producer) leaves together, after all copies were consumed
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// (n, p, q) float32 maps as a rank-3 tensor; box {TCB, rows, maps}; zero fill out of bounds.
+static bool make_map(CUtensorMap* tm, const float* base, int64_t n, int p, int q, int tcb, int rows, int maps) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)q, (cuuint64_t)p, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)q * 4, (cuuint64_t)p * q * 4};
+  cuuint32_t box[3] = {(cuuint32_t)tcb, (cuuint32_t)rows, (cuuint32_t)maps};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ----------------------------------------------------------------------------
@@ -805,7 +990,7 @@ namespace {
 struct LagLayout {
   Plan P;
   int nsplit;
-  size_t off_tasks, off_lane, off_boff, off_rec, off_Z, off_zoff, off_zlist, off_zones, off_msum, total;
+  size_t off_tasks, off_lane, off_boff, off_rec, off_Z, off_zoff, off_zlist, off_zones, off_msum, off_ids, total;
   int nzone_rec;  // total entries of zrec_list
 };
 
@@ -828,6 +1013,7 @@ static void lag_layout(const Geo& g, int nb, int64_t max_maps, int64_t n_maps, L
   L->off_zlist = take(sizeof(int) * L->P.nrec);
   L->off_zones = take(sizeof(int) * (2 * L->P.nrz + 2 * L->P.ncz + g.Hp + g.Wp));
   L->off_msum = take(sizeof(double) * 2 * (size_t)n_maps * g.d);
+  L->off_ids = take(sizeof(int) * L->P.tasks.size());
   L->total = o;
 }
 
@@ -928,7 +1114,8 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     A.batch_off = reinterpret_cast<const int64_t*>(w + L.off_boff);
     A.rec = reinterpret_cast<double*>(w + L.off_rec);
     A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
-    A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.nbatch = n_batches;
+    A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit;
+    A.nbatch = n_batches;
     A.xend = g.left + g.q;
     // F32: three float32 stages; else two float64 compute tiles + two float32 cp.async stages
     const size_t smem = (LAG_F32 ? 3 * sizeof(float) : 2 * sizeof(double) + 2 * sizeof(float)) * max_stage *
@@ -941,7 +1128,58 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       kern<<<grid, block, smem, st>>>(A);
     };
     const int tcv = TILE_X + P.NDX - 1;
-    if (g.l1 == 3 && tcv == 37) go(lag_zone_kernel<3, 37, LAG_F32>);
+    bool launched = false;
+    const bool use_tma = getenv("DDCCA_NO_TMA") == nullptr;
+    if (use_tma && (g.q % 4) == 0 && (g.l1 == 5 || g.l1 == 7 || g.l1 == 9) && g.l1 == g.l2) {
+      // box geometry: interior tasks stage slab+halo rows, short tasks L1 rows; widths padded to 4
+      TmaBoxes bx;
+      bx.rows_int = P.slab + g.l1 - 1;
+      bx.mb_int = std::max(1, std::min(8, STAGE_ROWS / bx.rows_int));
+      bx.rows_short = g.l1;
+      for (const Task& t : P.tasks)
+        if (t.y1 - t.y0 < g.l1) bx.rows_short = std::max(bx.rows_short, t.y1 - t.y0 + g.l1 - 1);
+      bx.mb_short = std::max(1, std::min(8, STAGE_ROWS / bx.rows_short));
+      const int x_first = g.left - (g.l2 - 1) - g.left;  // tile origin column of the first column tile
+      bx.shift = ((x_first % 4) + 4) % 4;
+      const int tcb = (tcv + bx.shift + 3) / 4 * 4;
+      CUtensorMap tm[4];
+      bool ok = true;
+      for (int v = 0; v < 2 && ok; ++v) {
+        const float* base = v == 0 ? maps1 : maps2;
+        ok = make_map(&tm[v], base, n_maps, g.p, g.q, tcb, bx.rows_int, bx.mb_int) &&
+             make_map(&tm[2 + v], base, n_maps, g.p, g.q, tcb, bx.rows_short, bx.mb_short);
+      }
+      if (ok) {
+        const size_t max_stage = (size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb;
+        const size_t tsmem = sizeof(float) * TMA_NS * max_stage + 2 * TMA_NS * sizeof(uint64_t);
+        dim3 tblock(32 * (P.G + 1));
+        // task ids by kind, uploaded after the plan tables
+        std::vector<int> ids_int, ids_short;
+        for (size_t t = 0; t < P.tasks.size(); ++t)
+          (P.tasks[t].y1 - P.tasks[t].y0 < g.l1 ? ids_short : ids_int).push_back((int)t);
+        int* ids_dev = reinterpret_cast<int*>(w + L.off_ids);
+        std::vector<int> ids_all(ids_int);
+        ids_all.insert(ids_all.end(), ids_short.begin(), ids_short.end());
+        cudaMemcpyAsync(ids_dev, ids_all.data(), sizeof(int) * ids_all.size(), cudaMemcpyHostToDevice, st);
+        auto tgo = [&](auto kern) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+          cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+          for (int v = 0; v < 2; ++v) {
+            if (!ids_int.empty())
+              kern<<<dim3((unsigned)ids_int.size(), (unsigned)L.nsplit, (unsigned)n_batches), tblock, tsmem, st>>>(
+                  A, bx, ids_dev, v, tm[v]);
+            if (!ids_short.empty())
+              kern<<<dim3((unsigned)ids_short.size(), (unsigned)L.nsplit, (unsigned)n_batches), tblock, tsmem, st>>>(
+                  A, bx, ids_dev + ids_int.size(), v, tm[2 + v]);
+          }
+        };
+        if (g.l1 == 5 && tcb == 40) { tgo(lag_tma_kernel<5, 40>); launched = true; }
+        else if (g.l1 == 7 && tcb == 48) { tgo(lag_tma_kernel<7, 48>); launched = true; }
+        else if (g.l1 == 9 && tcb == 52) { tgo(lag_tma_kernel<9, 52>); launched = true; }
+      }
+    }
+    if (launched) {
+    } else if (g.l1 == 3 && tcv == 37) go(lag_zone_kernel<3, 37, LAG_F32>);
     else if (g.l1 == 5 && tcv == 40) go(lag_zone_kernel<5, 40, LAG_F32>);
     else if (g.l1 == 7 && tcv == 46) go(lag_zone_kernel<7, 46, LAG_F32>);
     else if (g.l1 == 9 && tcv == 49) go(lag_zone_kernel<9, 49, LAG_F32>);

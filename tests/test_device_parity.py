@@ -339,3 +339,22 @@ def test_fused_conv_hist_matches_oracle(ex, l, count, p, q, bh, bw):
                      for i in range(b)])
     assert got.shape == want.shape
     assert np.mean(got == want) >= 0.999
+
+
+@pytest.mark.parametrize("l,p,q,nm", [(5, 28, 24, 3), (7, 40, 36, 2), (9, 33, 44, 2), (7, 9, 8, 1), (7, 130, 128, 1)])
+def test_tma_moments_path_matches_oracle(ex, l, p, q, nm, monkeypatch):
+    # q % 4 == 0 selects the TMA + mbarrier kernel; compare against the oracle and the cp.async kernel
+    rng = np.random.default_rng(l * 7 + q)
+    n, classes = 19, 5
+    m1 = rng.uniform(size=(n, nm, p, q)).astype(np.float32)
+    m2 = rng.standard_normal((n, nm, p, q)).astype(np.float32)
+    lab = rng.integers(0, classes, n)
+    geom = P.PatchGeometry(l, l)
+    out = P.LayerOutput(m1, m2, lab, tuple((i,) for i in range(nm)))
+    got = P.accumulate_layer_moments(out, geom, True, classes, P.BatchSpec(6), ex)
+    ref = oracle_acc(m1, m2, lab, geom, True, classes, 6)
+    assert rel(got.c11, ref.c11) <= 1e-11 and rel(got.c22, ref.c22) <= 1e-11
+    assert rel(got.class_sum1, ref.s1) <= 1e-11
+    monkeypatch.setenv("DDCCA_NO_TMA", "1")
+    alt = P.accumulate_layer_moments(out, geom, True, classes, P.BatchSpec(6), ex)
+    assert rel(got.c11, alt.c11) <= 1e-13 and rel(got.c22, alt.c22) <= 1e-13
