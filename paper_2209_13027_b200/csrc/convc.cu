@@ -13,9 +13,13 @@
 // the per-block histograms with warp-private shared bins, writing the counts
 // straight into the feature matrix. Codes never reach HBM.
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ddcca {
 
@@ -35,6 +39,7 @@ struct CArgs {
   int bh, bw, nby, nbx, br, kind, nbits;
   void* counts;
   int64_t gpr, row_stride, group_stride;
+  int use_tma;  // stage tiles with one cp.async.bulk.tensor per tile (else per-element cp.async)
 };
 
 __device__ __forceinline__ void cp_async4c(float* dst, const float* src, bool valid) {
@@ -42,117 +47,176 @@ __device__ __forceinline__ void cp_async4c(float* dst, const float* src, bool va
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 4 : 0));
 }
 
-__host__ __device__ inline int cc_tile_width(int cols, int l2, int px) {
+// Staged tile row: sh leading columns (so the TMA box origin is 16 B aligned), the
+// strips' inputs, and float4 over-read slack; a multiple of 4 floats.
+__host__ __device__ inline int cc_tile_width(int cols, int l2, int px, int sh) {
   const int G = (cols + px - 1) / px;
-  return ((G * px + l2 + 3) + 3) / 4 * 4;
+  return ((G * px + l2 + sh + 2) + 3) / 4 * 4;
 }
+// Tile buffer stride in floats (128 B aligned buffers for the TMA destination).
+__host__ __device__ inline int cc_buf_elems(int rows_in, int wt) { return (rows_in * wt + 31) / 32 * 32; }
 
-// PX x NF responses of the strip starting at tile row r0, column v0.
-template <int L1, int L2, int NF, int PX>
+// PY x PX x NF responses of the strip whose top-left output sits at tile row r0, column v0.
+// Each staged input row feeds the PY output rows it overlaps, so one row of x values
+// and one row of taps serve PY * PX * NF FFMAs.
+// Tile column v + SH holds padded column v.
+template <int L1, int L2, int NF, int PX, int PY, int SH>
 __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const float* __restrict__ tile, int Wt, int r0,
-                                         int v0, bool center, float (&acc)[PX][NF]) {
-  const float c = center ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + (L2 - 1) / 2] : 0.f;
+                                         int v0, bool center, float (&acc)[PY][PX][NF]) {
+  const float c = center ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + SH + (L2 - 1) / 2] : 0.f;
 #pragma unroll
-  for (int j = 0; j < PX; ++j)
+  for (int y = 0; y < PY; ++y)
 #pragma unroll
-    for (int g = 0; g < NF; ++g) acc[j][g] = 0.f;
+    for (int j = 0; j < PX; ++j)
+#pragma unroll
+      for (int g = 0; g < NF; ++g) acc[y][j][g] = 0.f;
   // rows stay rolled (keeps the loop body inside the instruction cache); taps of a
   // row are warp-uniform constant-bank loads feeding the FFMAs
 #pragma unroll 1
-  for (int a = 0; a < L1; ++a) {
+  for (int a = 0; a < L1 + PY - 1; ++a) {
     const float* row = tile + (r0 + a) * Wt + v0;
     constexpr int NX = PX + L2 - 1;
-    float x[(NX + 3) / 4 * 4];
+    constexpr int N4 = (NX + SH + 3) / 4;
+    float xr[4 * N4];
 #pragma unroll
-    for (int t4 = 0; t4 < (NX + 3) / 4; ++t4) {
+    for (int t4 = 0; t4 < N4; ++t4) {
       const float4 v = *reinterpret_cast<const float4*>(row + 4 * t4);
-      x[4 * t4 + 0] = v.x - c;
-      x[4 * t4 + 1] = v.y - c;
-      x[4 * t4 + 2] = v.z - c;
-      x[4 * t4 + 3] = v.w - c;
+      xr[4 * t4 + 0] = v.x;
+      xr[4 * t4 + 1] = v.y;
+      xr[4 * t4 + 2] = v.z;
+      xr[4 * t4 + 3] = v.w;
     }
+    float x[NX];
 #pragma unroll
-    for (int b = 0; b < L2; ++b)
+    for (int t = 0; t < NX; ++t) x[t] = xr[t + SH] - c;
 #pragma unroll
-      for (int g = 0; g < NF; ++g)
+    for (int y = 0; y < PY; ++y) {
+      const int ta = a - y;  // tap row of output row y that reads input row a
+      if (ta >= 0 && ta < L1) {
 #pragma unroll
-        for (int j = 0; j < PX; ++j) acc[j][g] = fmaf(T.w[(a * L2 + b) * NF + g], x[j + b], acc[j][g]);
+        for (int b = 0; b < L2; ++b)
+#pragma unroll
+          for (int g = 0; g < NF; ++g)
+#pragma unroll
+            for (int j = 0; j < PX; ++j)
+              acc[y][j][g] = fmaf(T.w[(ta * L2 + b) * NF + g], x[j + b], acc[y][j][g]);
+      }
+    }
   }
 }
 
-template <int NF, int PX>
-__device__ __forceinline__ unsigned cc_code(const float (&acc)[PX][NF], int j, int count) {
+template <int NF, int PX, int PY>
+__device__ __forceinline__ unsigned cc_code(const float (&acc)[PY][PX][NF], int y, int j, int count) {
   unsigned code = 0;
 #pragma unroll
   for (int g = 0; g < NF; ++g)
-    if (g < count && acc[j][g] > 0.f) code |= 1u << g;
+    if (g < count && acc[y][j][g] > 0.f) code |= 1u << g;
   return code;
 }
 
-// Stage rows [row0, row0 + rows) (padded coordinates) x tile columns [0, Wt) of map m.
-__device__ __forceinline__ void cc_issue(const CArgs& A, int64_t m, int row0, int rows, int Wt, float* buf) {
+// Stage rows [row0, row0 + rows) (padded coordinates) x tile columns [0, Wt) of map m,
+// tile column c = image column c - sh - left, zeros outside the map. TMA: thread 0
+// issues one box and arms the buffer's mbarrier; else every thread issues 4-byte
+// cp.async copies (one commit group per tile).
+__device__ __forceinline__ void cc_issue(const CArgs& A, const CUtensorMap* tm, uint64_t* bar, int sh, int64_t m,
+                                         int row0, int rows, int Wt, float* buf) {
+  if (A.use_tma) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, (unsigned)(rows * Wt * 4));
+      tma_load_3d(buf, tm, -(A.left + sh), row0 - A.top, (int)m, bar);
+    }
+    return;
+  }
   const float* img = A.in + m * (int64_t)A.p * A.q;
   for (int r = threadIdx.x >> 5; r < rows; r += CC_THREADS / 32) {
     const int i = row0 + r - A.top;
     const bool rok = i >= 0 && i < A.p;
     const float* rowp = img + (int64_t)i * A.q;
     for (int c = threadIdx.x & 31; c < Wt; c += 32) {
-      const int j = c - A.left;
+      const int j = c - sh - A.left;
       const bool ok = rok && j >= 0 && j < A.q;
       cp_async4c(buf + r * Wt + c, ok ? rowp + j : A.in, ok);
     }
   }
   asm volatile("cp.async.commit_group;\n" ::);
 }
+__device__ __forceinline__ void cc_commit_empty(const CArgs& A) {
+  if (!A.use_tma) asm volatile("cp.async.commit_group;\n" ::);
+}
+// Wait until the tile of iteration `it` sits in its buffer.
+__device__ __forceinline__ void cc_wait(const CArgs& A, uint64_t* bars, int it) {
+  if (A.use_tma) {
+    mbar_wait(&bars[it & 1], (unsigned)((it >> 1) & 1));
+  } else {
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+  }
+}
+__device__ __forceinline__ void cc_init_bars(const CArgs& A, uint64_t* bars) {
+  if (A.use_tma && threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+}
 
 // Persistent float-response conv (MODE 0): tiles = (map, band of rows_per_tile output rows).
-template <int L1, int L2, int NF, int PX>
-__global__ void __launch_bounds__(CC_THREADS) conv_c_kernel(CArgs A, Taps<L1 * L2 * NF> T) {
-  extern __shared__ __align__(16) float sm[];
+template <int L1, int L2, int NF, int PX, int PY, int SH>
+__global__ void __launch_bounds__(CC_THREADS)
+    conv_c_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) float sm[];
+  __shared__ uint64_t bars[2];
   const int G = (A.ow + PX - 1) / PX;
-  const int Wt = cc_tile_width(A.ow, L2, PX);
-  const int rows_out = max(1, CC_THREADS / G);  // output rows per tile (one strip per thread)
+  const int Wt = cc_tile_width(A.ow, L2, PX, SH);
+  const int rows_out = PY * max(1, CC_THREADS / G);  // output rows per tile (one strip per thread)
   const int rows_in = rows_out + L1 - 1;
   const int bands = (A.oh + rows_out - 1) / rows_out;
   const int64_t total = A.n_maps * bands;
   float* bufs = sm;
-  const int belems = rows_in * Wt;
+  const int belems = cc_buf_elems(rows_in, Wt);
+  cc_init_bars(A, bars);
   int64_t t = blockIdx.x;
-  if (t < total) cc_issue(A, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
+  if (t < total) cc_issue(A, &tmap, &bars[0], SH, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
   const int64_t plane = (int64_t)A.oh * A.ow;
   for (int it = 0; t < total; t += gridDim.x, ++it) {
     const float* cur = bufs + (it & 1) * belems;
     const int64_t tn = t + gridDim.x;
     if (tn < total)
-      cc_issue(A, tn / bands, (int)(tn % bands) * rows_out, rows_in, Wt, bufs + ((it + 1) & 1) * belems);
+      cc_issue(A, &tmap, &bars[(it + 1) & 1], SH, tn / bands, (int)(tn % bands) * rows_out, rows_in, Wt,
+               bufs + ((it + 1) & 1) * belems);
     else
-      asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);
-    __syncthreads();
+      cc_commit_empty(A);
+    cc_wait(A, bars, it);
     const int64_t m = t / bands;
     const int u0 = (int)(t % bands) * rows_out;
-    const int r = threadIdx.x / G, gi = threadIdx.x % G;
-    const int u = u0 + r;
-    if (r < rows_out && u < A.oh) {
+    const int r = threadIdx.x / G * PY, gi = threadIdx.x % G;
+    if (r < rows_out && u0 + r < A.oh) {
       const int v0 = gi * PX;
-      float acc[PX][NF];
-      cc_strip<L1, L2, NF, PX>(T, cur, Wt, r, v0, A.center, acc);
-      float* o = static_cast<float*>(A.out) + m * A.count * plane + (int64_t)u * A.ow + v0;
-      if (v0 + PX <= A.ow && (A.ow & 3) == 0 && PX % 4 == 0) {
+      float acc[PY][PX][NF];
+      cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
 #pragma unroll
-        for (int g = 0; g < NF; ++g)
-          if (g < A.count)
+      for (int y = 0; y < PY; ++y) {
+        const int u = u0 + r + y;
+        if (u >= A.oh) break;
+        float* o = static_cast<float*>(A.out) + m * A.count * plane + (int64_t)u * A.ow + v0;
+        if (v0 + PX <= A.ow && (A.ow & 3) == 0 && PX % 4 == 0) {
 #pragma unroll
-            for (int j4 = 0; j4 < PX / 4; ++j4)
-              *reinterpret_cast<float4*>(o + g * plane + 4 * j4) =
-                  make_float4(acc[4 * j4][g], acc[4 * j4 + 1][g], acc[4 * j4 + 2][g], acc[4 * j4 + 3][g]);
-      } else {
+          for (int g = 0; g < NF; ++g)
+            if (g < A.count)
 #pragma unroll
-        for (int j = 0; j < PX; ++j)
-          if (v0 + j < A.ow)
+              for (int j4 = 0; j4 < PX / 4; ++j4)
+                *reinterpret_cast<float4*>(o + g * plane + 4 * j4) = make_float4(
+                    acc[y][4 * j4][g], acc[y][4 * j4 + 1][g], acc[y][4 * j4 + 2][g], acc[y][4 * j4 + 3][g]);
+        } else {
 #pragma unroll
-            for (int g = 0; g < NF; ++g)
-              if (g < A.count) o[g * plane + j] = acc[j][g];
+          for (int j = 0; j < PX; ++j)
+            if (v0 + j < A.ow)
+#pragma unroll
+              for (int g = 0; g < NF; ++g)
+                if (g < A.count) o[g * plane + j] = acc[y][j][g];
+        }
       }
     }
     __syncthreads();
@@ -160,15 +224,17 @@ __global__ void __launch_bounds__(CC_THREADS) conv_c_kernel(CArgs A, Taps<L1 * L
 }
 
 // Fused last layer: codes of BR block-rows in shared memory -> block histograms -> counts.
-template <int L1, int L2, int NF, int PX>
-__global__ void __launch_bounds__(CC_THREADS) conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T) {
-  extern __shared__ __align__(16) float sm[];
+template <int L1, int L2, int NF, int PX, int PY, int SH>
+__global__ void __launch_bounds__(CC_THREADS)
+    conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) float sm[];
+  __shared__ uint64_t bars[2];
   const int cols = A.nbx * A.bw;                 // only pixels inside blocks are needed
   const int G = (cols + PX - 1) / PX;
-  const int Wt = cc_tile_width(cols, L2, PX);
+  const int Wt = cc_tile_width(cols, L2, PX, SH);
   const int rows_out = A.br * A.bh;
-  const int rows_in = rows_out + L1 - 1;
-  const int belems = rows_in * Wt;
+  const int rows_in = (rows_out + PY - 1) / PY * PY + L1 - 1;
+  const int belems = cc_buf_elems(rows_in, Wt);
   const int bands = (A.nby + A.br - 1) / A.br;
   const int64_t total = A.n_maps * bands;
   const int nbins = 1 << A.nbits;
@@ -178,28 +244,45 @@ __global__ void __launch_bounds__(CC_THREADS) conv_hist_kernel(CArgs A, Taps<L1 
   uint16_t* codes = reinterpret_cast<uint16_t*>(bufs + 2 * belems);  // [rows_out][cols]
   unsigned* bins = reinterpret_cast<unsigned*>(codes + ((rows_out * cols + 1) & ~1));  // [nwarps][words]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  cc_init_bars(A, bars);
   int64_t t = blockIdx.x;
-  if (t < total) cc_issue(A, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
+  if (t < total) cc_issue(A, &tmap, &bars[0], SH, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
   for (int it = 0; t < total; t += gridDim.x, ++it) {
     const float* cur = bufs + (it & 1) * belems;
     const int64_t tn = t + gridDim.x;
     if (tn < total)
-      cc_issue(A, tn / bands, (int)(tn % bands) * rows_out, rows_in, Wt, bufs + ((it + 1) & 1) * belems);
+      cc_issue(A, &tmap, &bars[(it + 1) & 1], SH, tn / bands, (int)(tn % bands) * rows_out, rows_in, Wt,
+               bufs + ((it + 1) & 1) * belems);
     else
-      asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 1;\n" ::);
-    __syncthreads();
+      cc_commit_empty(A);
+    cc_wait(A, bars, it);
     const int64_t m = t / bands;
     const int by0 = (int)(t % bands) * A.br;
     const int nbr = min(A.br, A.nby - by0);      // block rows in this band
     // 1) codes of the band into shared memory
-    for (int s = threadIdx.x; s < nbr * A.bh * G; s += CC_THREADS) {
-      const int r = s / G, v0 = (s % G) * PX;
-      float acc[PX][NF];
-      cc_strip<L1, L2, NF, PX>(T, cur, Wt, r, v0, A.center, acc);
+    const int band_rows = nbr * A.bh;
+    for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += CC_THREADS) {
+      const int r = s / G * PY, v0 = (s % G) * PX;
+      float acc[PY][PX][NF];
+      cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
 #pragma unroll
-      for (int j = 0; j < PX; ++j)
-        if (v0 + j < cols) codes[r * cols + v0 + j] = (uint16_t)cc_code<NF, PX>(acc, j, A.count);
+      for (int y = 0; y < PY; ++y)
+        if (r + y < band_rows) {
+          if (PX % 4 == 0 && v0 + PX <= cols && (cols & 3) == 0) {
+#pragma unroll
+            for (int j4 = 0; j4 < PX / 4; ++j4) {
+              uint2 w;
+              w.x = cc_code<NF, PX, PY>(acc, y, 4 * j4, A.count) | cc_code<NF, PX, PY>(acc, y, 4 * j4 + 1, A.count) << 16;
+              w.y = cc_code<NF, PX, PY>(acc, y, 4 * j4 + 2, A.count) |
+                    cc_code<NF, PX, PY>(acc, y, 4 * j4 + 3, A.count) << 16;
+              *reinterpret_cast<uint2*>(codes + (r + y) * cols + v0 + 4 * j4) = w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < PX; ++j)
+              if (v0 + j < cols) codes[(r + y) * cols + v0 + j] = (uint16_t)cc_code<NF, PX, PY>(acc, y, j, A.count);
+          }
+        }
     }
     __syncthreads();
     // 2) one warp per block: warp-private bins, counts out
@@ -208,10 +291,21 @@ __global__ void __launch_bounds__(CC_THREADS) conv_hist_kernel(CArgs A, Taps<L1 
       const int rb = blk / A.nbx, bx = blk % A.nbx;
       for (int w = lane; w < words; w += 32) wb[w] = 0u;
       __syncwarp();
-      for (int px = lane; px < A.bh * A.bw; px += 32) {
-        const int r = rb * A.bh + px / A.bw, c = bx * A.bw + px % A.bw;
-        const unsigned code = codes[r * cols + c];
-        atomicAdd(&wb[code >> 1], 1u << ((code & 1u) * 16));
+      const uint16_t* cb = codes + rb * A.bh * cols + bx * A.bw;
+      if (A.bw <= 32) {
+        // lanes tile (32 / bw) rows x bw columns per step
+        const int per = 32 / A.bw, lr = lane / A.bw, lc = lane - lr * A.bw;
+        if (lr < per)
+          for (int r = lr; r < A.bh; r += per) {
+            const unsigned code = cb[r * cols + lc];
+            atomicAdd(&wb[code >> 1], 1u << ((code & 1u) * 16));
+          }
+      } else {
+        for (int r = 0; r < A.bh; ++r)
+          for (int c = lane; c < A.bw; c += 32) {
+            const unsigned code = cb[r * cols + c];
+            atomicAdd(&wb[code >> 1], 1u << ((code & 1u) * 16));
+          }
       }
       __syncwarp();
       const int64_t blk_global = (int64_t)(by0 + rb) * A.nbx + bx;
@@ -273,61 +367,95 @@ static int persistent_grid(K kern, size_t smem, int64_t tiles) {
   return (int)grid;
 }
 
-template <int L1, int L2, int NF, int PX>
-static int run_conv_c(const CArgs& A, const float* pack_host, cudaStream_t st) {
+// TMA staging needs 16 B aligned rows (q % 4 == 0) and a box of at most 256 x 256;
+// DDCCA_NO_TMA=1 forces the cp.async path (A/B checks).
+static bool cc_tma_map(CArgs& A, int sh, int Wt, int rows_in, CUtensorMap* tm) {
+  const char* env = getenv("DDCCA_NO_TMA");
+  const bool disabled = env && env[0] == '1';
+  memset(tm, 0, sizeof(*tm));
+  A.use_tma = 0;
+  if (disabled || (A.left + sh) % 4 != 0 || A.q % 4 != 0 || Wt > 256 || rows_in > 256 || (reinterpret_cast<uintptr_t>(A.in) & 15) ||
+      A.n_maps > INT32_MAX)
+    return false;
+  A.use_tma = make_map(tm, A.in, A.n_maps, A.p, A.q, Wt, rows_in, 1) ? 1 : 0;
+  return A.use_tma != 0;
+}
+
+template <int L1, int L2, int NF, int PX, int PY, int SH>
+static int run_conv_c(CArgs A, const float* pack_host, cudaStream_t st) {
   Taps<L1 * L2 * NF> T;
   zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
   const int G = (A.ow + PX - 1) / PX;
-  const int Wt = cc_tile_width(A.ow, L2, PX);
-  const int rows_out = std::max(1, CC_THREADS / G);
+  const int Wt = cc_tile_width(A.ow, L2, PX, SH);
+  const int rows_out = PY * std::max(1, CC_THREADS / G);
   const int rows_in = rows_out + L1 - 1;
-  const size_t smem = sizeof(float) * 2 * (size_t)rows_in * Wt;
+  CUtensorMap tm;
+  if (SH != 0 && !cc_tma_map(A, SH, Wt, rows_in, &tm)) return DDCCA_ECONFIG;  // caller retries with SH = 0
+  if (SH == 0) cc_tma_map(A, SH, Wt, rows_in, &tm);
+  const size_t smem = sizeof(float) * 2 * (size_t)cc_buf_elems(rows_in, Wt);
   if (smem > 200 * 1024) return fail(DDCCA_ECONFIG, "conv: map row too wide for shared-memory staging");
   const int64_t tiles = A.n_maps * ((A.oh + rows_out - 1) / rows_out);
-  auto kern = conv_c_kernel<L1, L2, NF, PX>;
+  auto kern = conv_c_kernel<L1, L2, NF, PX, PY, SH>;
   const int grid = persistent_grid(kern, smem, tiles);
-  kern<<<grid, CC_THREADS, smem, st>>>(A, T);
+  kern<<<grid, CC_THREADS, smem, st>>>(A, T, tm);
   return check_launch("conv_c_kernel");
 }
 
-template <int L1, int L2, int NF, int PX>
+template <int L1, int L2, int NF, int PX, int PY, int SH>
 static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
   Taps<L1 * L2 * NF> T;
   zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
   const int cols = A.nbx * A.bw;
   const int G = (cols + PX - 1) / PX;
   // block rows per CTA: about one strip per thread, at least one block row
-  A.br = std::max(1, std::min(A.nby, CC_THREADS / std::max(1, A.bh * G)));
+  A.br = std::max(1, std::min(A.nby, PY * CC_THREADS / std::max(1, A.bh * G)));
   const int rows_out = A.br * A.bh;
-  const int Wt = cc_tile_width(cols, L2, PX);
-  const int rows_in = rows_out + L1 - 1;
+  const int Wt = cc_tile_width(cols, L2, PX, SH);
+  const int rows_in = (rows_out + PY - 1) / PY * PY + L1 - 1;
+  CUtensorMap tm;
+  if (SH != 0 && !cc_tma_map(A, SH, Wt, rows_in, &tm)) return DDCCA_ECONFIG;
+  if (SH == 0) cc_tma_map(A, SH, Wt, rows_in, &tm);
   const int nbins = 1 << A.nbits;
-  const size_t smem = sizeof(float) * 2 * (size_t)rows_in * Wt + sizeof(uint16_t) * (((size_t)rows_out * cols + 1) & ~1ull) +
+  const size_t smem = sizeof(float) * 2 * (size_t)cc_buf_elems(rows_in, Wt) +
+                      sizeof(uint16_t) * (((size_t)rows_out * cols + 1) & ~1ull) +
                       sizeof(unsigned) * (CC_THREADS / 32) * (size_t)((nbins + 1) / 2);
   if (smem > 220 * 1024) return fail(DDCCA_ECONFIG, "conv_hist: band does not fit shared memory");
   const int64_t tiles = A.n_maps * ((A.nby + A.br - 1) / A.br);
-  auto kern = conv_hist_kernel<L1, L2, NF, PX>;
+  auto kern = conv_hist_kernel<L1, L2, NF, PX, PY, SH>;
   const int grid = persistent_grid(kern, smem, tiles);
-  kern<<<grid, CC_THREADS, smem, st>>>(A, T);
+  kern<<<grid, CC_THREADS, smem, st>>>(A, T, tm);
   return check_launch("conv_hist_kernel");
+}
+
+// Column shift that 16 B aligns the TMA box origin -(left + sh) for "same" padding.
+constexpr int same_shift(int l2) { return (4 - ((l2 - 1) / 2) % 4) % 4; }
+
+template <bool HIST, int L, int NF, int PX, int PY>
+static int run_shape(const CArgs& A, const float* pack_host, cudaStream_t st) {
+  constexpr int S = same_shift(L);
+  const int want = (4 - A.left % 4) % 4;
+  if (S != 0 && want == S) {
+    const int rc = HIST ? run_conv_hist<L, L, NF, PX, PY, S>(A, pack_host, st) : run_conv_c<L, L, NF, PX, PY, S>(A, pack_host, st);
+    if (rc != DDCCA_ECONFIG) return rc;
+  }
+  return HIST ? run_conv_hist<L, L, NF, PX, PY, 0>(A, pack_host, st) : run_conv_c<L, L, NF, PX, PY, 0>(A, pack_host, st);
 }
 
 // Dispatch over the compiled (window, filter-count) shapes; DDCCA_ECONFIG = not covered.
 template <bool HIST>
 static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cudaStream_t st) {
-#define DDCCA_CC(L, NFV, PXV)                                                                                \
-  if (l1 == L && l2 == L && A.count <= NFV)                                                                  \
-    return HIST ? run_conv_hist<L, L, NFV, PXV>(A, pack_host, st) : run_conv_c<L, L, NFV, PXV>(A, pack_host, st);
-  DDCCA_CC(3, 8, 8)
-  DDCCA_CC(5, 8, 8)
-  DDCCA_CC(7, 8, 8)
-  DDCCA_CC(9, 8, 8)
-  DDCCA_CC(3, 16, 4)
-  DDCCA_CC(5, 16, 4)
-  DDCCA_CC(7, 12, 4)
-  DDCCA_CC(7, 16, 4)
-  DDCCA_CC(9, 12, 4)
-  DDCCA_CC(9, 16, 4)
+#define DDCCA_CC(L, NFV, PXV, PYV) \
+  if (l1 == L && l2 == L && A.count <= NFV) return run_shape<HIST, L, NFV, PXV, PYV>(A, pack_host, st);
+  DDCCA_CC(3, 8, 8, 1)
+  DDCCA_CC(5, 8, 8, 1)
+  DDCCA_CC(7, 8, 8, 1)
+  DDCCA_CC(9, 8, 8, 1)
+  DDCCA_CC(3, 16, 4, 1)
+  DDCCA_CC(5, 16, 4, 1)
+  DDCCA_CC(7, 12, 4, 1)
+  DDCCA_CC(7, 16, 4, 1)
+  DDCCA_CC(9, 12, 4, 1)
+  DDCCA_CC(9, 16, 4, 1)
 #undef DDCCA_CC
   return fail(DDCCA_ECONFIG, "no constant-bank conv instance for %dx%d with %d filters", l1, l2, A.count);
 }

@@ -341,6 +341,51 @@ def test_fused_conv_hist_matches_oracle(ex, l, count, p, q, bh, bw):
     assert np.mean(got == want) >= 0.999
 
 
+@pytest.mark.parametrize("l,count,p,q,padding", [(7, 8, 40, 36, "zero_same"), (3, 8, 16, 20, "zero_same"),
+                                                 (5, 8, 28, 24, "zero_same"), (9, 12, 32, 40, "zero_same"),
+                                                 (7, 8, 40, 36, "none"), (5, 16, 64, 128, "zero_same")])
+def test_tma_conv_paths_bitwise(ex, l, count, p, q, padding, monkeypatch):
+    """TMA-staged tiles (q % 4 == 0) and per-element cp.async staging give identical bits; both match the oracle."""
+    rng = np.random.default_rng(l * 7 + q)
+    stack = rng.uniform(size=(6, p, q)).astype(np.float32)
+    f = rng.standard_normal((count, l, l))
+    geom = P.PatchGeometry(l, l, 1, padding)
+    dev = torch.from_numpy(stack).to(ex.device)
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, geom, True)
+        got = E.conv(ex, dev, lay, 1).cpu().numpy()
+        monkeypatch.setenv("DDCCA_NO_TMA", "1")
+        alt = E.conv(ex, dev, lay, 1).cpu().numpy()
+        monkeypatch.delenv("DDCCA_NO_TMA")
+    assert np.array_equal(got, alt)
+    ref = O.conv_stack(stack, O.Layer(f, f, O.Geometry(l, l, 1, padding), True), 1)
+    scale = np.abs(f).sum(axis=(1, 2)).max()
+    assert np.abs(got - ref).max() <= 3e-6 * scale
+
+
+@pytest.mark.parametrize("l,count,p,q,bh,bw", [(7, 8, 64, 48, 16, 16), (5, 8, 28, 24, 7, 6), (9, 12, 40, 40, 8, 8),
+                                               (3, 4, 16, 20, 4, 5), (7, 8, 128, 128, 16, 16)])
+def test_tma_conv_hist_paths_identical(ex, l, count, p, q, bh, bw, monkeypatch):
+    rng = np.random.default_rng(l + q + bw)
+    n_in, b = 2, 3
+    maps = torch.from_numpy(rng.standard_normal((b * n_in, p, q)).astype(np.float32)).to(ex.device)
+    f = rng.standard_normal((count, l, l))
+    geom = P.PatchGeometry(l, l)
+    plan = E.block_plan(P.EncoderConfig(bh, bw), p, q, count)
+    kind = E.count_kind(plan.bpc)
+    featlen = n_in * plan.blocks * plan.bins
+    outs = []
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, geom, True)
+        for env in ("0", "1"):
+            monkeypatch.setenv("DDCCA_NO_TMA", env)
+            out = torch.zeros((b, featlen), dtype=torch.int16 if kind == 2 else torch.uint8, device=ex.device)
+            assert E.conv_hist(ex, maps, lay, 1, plan, out.view(-1), kind, n_in, featlen, plan.blocks * plan.bins)
+            outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    assert outs[0].any()
+
+
 @pytest.mark.parametrize("l,p,q,nm", [(5, 28, 24, 3), (7, 40, 36, 2), (9, 33, 44, 2), (7, 9, 8, 1), (7, 130, 128, 1)])
 def test_tma_moments_path_matches_oracle(ex, l, p, q, nm, monkeypatch):
     # q % 4 == 0 selects the TMA + mbarrier kernel; compare against the oracle and the cp.async kernel
