@@ -26,7 +26,7 @@ namespace ddcca {
 constexpr int CC_THREADS = 256;
 
 template <int N>
-struct Taps {
+struct alignas(16) Taps {
   float w[N];
 };
 

@@ -180,16 +180,16 @@ struct LagArgs {
 // whole ring turns of L1; rows >= nrows are masked through the own value
 // (their staged data is still valid partner data for earlier rows). TC > 0
 // makes the tile stride a compile-time constant (all smem offsets immediate).
-template <int L1, int TC, bool SKIP0, typename S>
+template <int L1, int TC, bool SKIP0, int KK, typename S>
 __device__ __forceinline__ void lag_accumulate(const S* __restrict__ t, int tc_rt, int nrows, int cown,
                                                int cpart, double (&acc)[L1][KDX]) {
   const int tc = TC > 0 ? TC : tc_rt;
-  double ring[L1][KDX];
+  double ring[L1][KK];
   const S* pp = t + cpart;
 #pragma unroll
   for (int q = 0; q < L1 - 1; ++q)
 #pragma unroll
-    for (int k = 0; k < KDX; ++k) ring[q][k] = (double)pp[q * tc + k];
+    for (int k = 0; k < KK; ++k) ring[q][k] = (double)pp[q * tc + k];
   pp += (L1 - 1) * tc;
   const S* po = t + cown;
   for (int r0 = 0; r0 < nrows; r0 += L1) {
@@ -197,13 +197,13 @@ __device__ __forceinline__ void lag_accumulate(const S* __restrict__ t, int tc_r
     for (int u = 0; u < L1; ++u) {
       const int snew = (u + L1 - 1) % L1;
 #pragma unroll
-      for (int k = 0; k < KDX; ++k) ring[snew][k] = (double)pp[u * tc + k];
+      for (int k = 0; k < KK; ++k) ring[snew][k] = (double)pp[u * tc + k];
       double own = (double)po[u * tc];
       own = (r0 + u < nrows) ? own : 0.0;
 #pragma unroll
       for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy)
 #pragma unroll
-        for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, ring[(u + dy) % L1][k], acc[dy][k]);
+        for (int k = 0; k < KK; ++k) acc[dy][k] = fma(own, ring[(u + dy) % L1][k], acc[dy][k]);
     }
     pp += L1 * tc;
     po += L1 * tc;
@@ -211,7 +211,7 @@ __device__ __forceinline__ void lag_accumulate(const S* __restrict__ t, int tc_r
 }
 
 // Tasks shorter than one ring turn (the single border rows): direct partner loads.
-template <int L1, int TC, typename S>
+template <int L1, int TC, int KK, typename S>
 __device__ __forceinline__ void lag_accumulate_short(const S* __restrict__ t, int tc_rt, int nrows, int cown,
                                                      int cpart, bool skip0, double (&acc)[L1][KDX]) {
   const int tc = TC > 0 ? TC : tc_rt;
@@ -222,8 +222,29 @@ __device__ __forceinline__ void lag_accumulate_short(const S* __restrict__ t, in
     for (int dy = 0; dy < L1; ++dy) {
       if (dy == 0 && skip0) continue;
 #pragma unroll
-      for (int k = 0; k < KDX; ++k) acc[dy][k] = fma(own, (double)pp[dy * tc + k], acc[dy][k]);
+      for (int k = 0; k < KK; ++k) acc[dy][k] = fma(own, (double)pp[dy * tc + k], acc[dy][k]);
     }
+  }
+}
+
+// One staged map tile through this warp's lag group. kk = live dx lags of the group
+// (the last group of 2*l2-1 lags may be partial: its padding lags are not computed).
+template <int L1, int TC, typename S>
+__device__ __forceinline__ void lag_map(const S* __restrict__ t, int tc, int nrows, int cown, int cpart,
+                                        bool short_task, bool skip0, int kk, double (&acc)[L1][KDX]) {
+  static_assert(KDX == 3, "lag_map dispatches 1..3 live lags");
+  if (short_task) {
+    if (kk >= 3) lag_accumulate_short<L1, TC, 3>(t, tc, nrows, cown, cpart, skip0, acc);
+    else if (kk == 2) lag_accumulate_short<L1, TC, 2>(t, tc, nrows, cown, cpart, skip0, acc);
+    else lag_accumulate_short<L1, TC, 1>(t, tc, nrows, cown, cpart, skip0, acc);
+  } else if (skip0) {
+    lag_accumulate<L1, TC, true, 3>(t, tc, nrows, cown, cpart, acc);
+  } else if (kk >= 3) {
+    lag_accumulate<L1, TC, false, 3>(t, tc, nrows, cown, cpart, acc);
+  } else if (kk == 2) {
+    lag_accumulate<L1, TC, false, 2>(t, tc, nrows, cown, cpart, acc);
+  } else {
+    lag_accumulate<L1, TC, false, 1>(t, tc, nrows, cown, cpart, acc);
   }
 }
 
@@ -309,6 +330,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   const int cpart = lane + grp * KDX;  // partner column of k = 0
   // groups whose dx are all negative skip the dy = 0 lag (canonical half-plane only)
   const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
+  const int kk = min(KDX, 2 * A.l2 - 1 - grp * KDX);  // live lags of this group
 
   if constexpr (F32) {
     if (ma < mbnd) issue(ma, raw); else asm volatile("cp.async.commit_group;\n" ::);
@@ -325,12 +347,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
       const int nm = (int)min((int64_t)mb, mbnd - ms);
       for (int j = 0; j < nm; ++j) {
         const float* t = tile + j * tile_elems;
-        if (short_task)
-          lag_accumulate_short<L1, TC>(t, tc, nrows, cown, cpart, skip0, acc);
-        else if (skip0)
-          lag_accumulate<L1, TC, true>(t, tc, nrows, cown, cpart, acc);
-        else
-          lag_accumulate<L1, TC, false>(t, tc, nrows, cown, cpart, acc);
+        lag_map<L1, TC>(t, tc, nrows, cown, cpart, short_task, skip0, kk, acc);
       }
     }
   } else {
@@ -348,12 +365,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
     const int nm = (int)min((int64_t)mb, mbnd - ms);
     for (int j = 0; j < nm; ++j) {
       const double* t = tile + j * tile_elems;
-      if (short_task)
-        lag_accumulate_short<L1, TC>(t, tc, nrows, cown, cpart, skip0, acc);
-      else if (skip0)
-        lag_accumulate<L1, TC, true>(t, tc, nrows, cown, cpart, acc);
-      else
-        lag_accumulate<L1, TC, false>(t, tc, nrows, cown, cpart, acc);
+      lag_map<L1, TC>(t, tc, nrows, cown, cpart, short_task, skip0, kk, acc);
     }
   }
   }
@@ -382,12 +394,18 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
 // mbarrier and release it through its "empty" mbarrier. No __syncthreads and
 // no per-element staging instructions in the steady state.
 // ----------------------------------------------------------------------------
-constexpr int TMA_NS = 3;
+constexpr int TMA_NS = 3;  // default ring depth (DDCCA_TMA_STAGES overrides, 2..8)
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
 
 struct TmaBoxes {
   int rows_int, mb_int;      // interior tasks (nrows >= L1)
   int rows_short, mb_short;  // short (single border row) tasks
   int shift;                 // columns the tile starts early so the box origin is 16 B aligned
+  int ns;                    // ring depth (stages in flight)
 };
 
 // One launch per (view, task kind): the single tensor map is used directly from
@@ -410,8 +428,9 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
   const int tile_elems = trb * TCB;
   const int stage_elems = mb * tile_elems;
   const int max_stage = max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * TCB;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_mem + TMA_NS * max_stage);
-  uint64_t* empty = full + TMA_NS;
+  const int NS = bx.ns;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_mem + NS * max_stage);
+  uint64_t* empty = full + NS;
   const int64_t m_begin = A.batch_off[batch];
   const int64_t m_end = A.batch_off[batch + 1];
   const int64_t per = (m_end - m_begin + A.nsplit - 1) / A.nsplit;
@@ -420,7 +439,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
   const int nstages = ma < mbnd ? (int)((mbnd - ma + mb - 1) / mb) : 0;
   const int G = A.G;  // consumer warps; warp G is the producer
   if (threadIdx.x == 0) {
-    for (int i = 0; i < TMA_NS; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], G);
     }
@@ -437,8 +456,8 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
     const int y = T.y0 - A.top;                 // image row of tile row 0
     const unsigned bytes = (unsigned)stage_elems * 4u;
     for (int s = 0; s < nstages; ++s) {
-      const int slot = s % TMA_NS;
-      if (s >= TMA_NS) mbar_wait(&empty[slot], (unsigned)((s / TMA_NS - 1) & 1));
+      const int slot = s % NS;
+      if (s >= NS) mbar_wait(&empty[slot], (unsigned)((s / NS - 1) & 1));
       if (lane == 0) {
         mbar_expect_tx(&full[slot], bytes);
         tma_load_3d(stage_mem + slot * max_stage, &tmap, x, y, (int)(ma + (int64_t)s * mb), &full[slot]);
@@ -455,20 +474,16 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
     const int cown = lane + (A.l2 - 1) + bx.shift;
     const int cpart = lane + grp * KDX + bx.shift;
     const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
+    const int kk = min(KDX, 2 * A.l2 - 1 - grp * KDX);  // live lags of this group
     for (int s = 0; s < nstages; ++s) {
-      const int slot = s % TMA_NS;
-      mbar_wait(&full[slot], (unsigned)((s / TMA_NS) & 1));
+      const int slot = s % NS;
+      mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
       const float* tile = stage_mem + slot * max_stage;
       const int64_t ms = ma + (int64_t)s * mb;
       const int nm = (int)min((int64_t)mb, mbnd - ms);
       for (int j = 0; j < nm; ++j) {
         const float* t = tile + j * tile_elems;
-        if (short_task)
-          lag_accumulate_short<L1, TCB>(t, TCB, nrows, cown, cpart, skip0, acc);
-        else if (skip0)
-          lag_accumulate<L1, TCB, true>(t, TCB, nrows, cown, cpart, acc);
-        else
-          lag_accumulate<L1, TCB, false>(t, TCB, nrows, cown, cpart, acc);
+        lag_map<L1, TCB>(t, TCB, nrows, cown, cpart, short_task, skip0, kk, acc);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -1070,12 +1085,14 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
     if (use_tma && (g.q % 4) == 0 && (g.l1 == 5 || g.l1 == 7 || g.l1 == 9) && g.l1 == g.l2) {
       // box geometry: interior tasks stage slab+halo rows, short tasks L1 rows; widths padded to 4
       TmaBoxes bx;
+      const int stage_rows = env_int("DDCCA_TMA_ROWS", STAGE_ROWS);
+      bx.ns = std::max(2, std::min(8, env_int("DDCCA_TMA_STAGES", TMA_NS)));
       bx.rows_int = P.slab + g.l1 - 1;
-      bx.mb_int = std::max(1, std::min(8, STAGE_ROWS / bx.rows_int));
+      bx.mb_int = std::max(1, std::min(8, stage_rows / bx.rows_int));
       bx.rows_short = g.l1;
       for (const Task& t : P.tasks)
         if (t.y1 - t.y0 < g.l1) bx.rows_short = std::max(bx.rows_short, t.y1 - t.y0 + g.l1 - 1);
-      bx.mb_short = std::max(1, std::min(8, STAGE_ROWS / bx.rows_short));
+      bx.mb_short = std::max(1, std::min(8, stage_rows / bx.rows_short));
       const int x_first = g.left - (g.l2 - 1) - g.left;  // tile origin column of the first column tile
       bx.shift = ((x_first % 4) + 4) % 4;
       const int tcb = (tcv + bx.shift + 3) / 4 * 4;
@@ -1088,7 +1105,7 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       }
       if (ok) {
         const size_t max_stage = (size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb;
-        const size_t tsmem = sizeof(float) * TMA_NS * max_stage + 2 * TMA_NS * sizeof(uint64_t);
+        const size_t tsmem = sizeof(float) * bx.ns * max_stage + 2 * bx.ns * sizeof(uint64_t);
         dim3 tblock(32 * (P.G + 1));
         // task ids by kind, uploaded after the plan tables
         std::vector<int> ids_int, ids_short;

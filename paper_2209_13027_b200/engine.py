@@ -33,6 +33,8 @@ from .patches import PatchGeometry
 
 MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
 KEEP_MAPS_BYTES = 48 << 30  # fit keeps the last layer's input maps (both views) for the transform if they fit
+HOST_CHUNK_BATCHES = 12  # sample batches per streamed device->host count copy
+
 
 
 def _torch():
@@ -510,6 +512,9 @@ class Engine:
         per_view = groups * plan.blocks * plan.bins
         per_sample = max(groups * pm * qm * 4, featlen * (2 if kind == 2 else 1) if sink is not None else 0)
         supers = self._superbatches(ranges, per_sample)
+        if host_out is not None:
+            # small groups so each group's device->host copy overlaps the next group's kernels
+            supers = [g[i:i + HOST_CHUNK_BATCHES] for g in supers for i in range(0, len(g), HOST_CHUNK_BATCHES)]
         if out is None:
             rows = max(g[-1].stop - g[0].start for g in supers) if sink is not None else m
             out = torch.empty((rows, featlen), dtype=dt, device=ex.device)
