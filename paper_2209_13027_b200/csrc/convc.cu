@@ -223,7 +223,9 @@ __global__ void __launch_bounds__(CC_THREADS)
   }
 }
 
-// Fused last layer: codes of BR block-rows in shared memory -> block histograms -> counts.
+// Fused last layer: sign codes of BR block-rows go straight into per-block shared
+// bins (packed u16 pairs, CTA-wide atomics); then one warp per block writes the
+// counts into the feature row and clears the bins.
 template <int L1, int L2, int NF, int PX, int PY, int SH>
 __global__ void __launch_bounds__(CC_THREADS)
     conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
@@ -240,10 +242,10 @@ __global__ void __launch_bounds__(CC_THREADS)
   const int nbins = 1 << A.nbits;
   const int words = (nbins + 1) / 2;
   const int nwarps = CC_THREADS / 32;
-  float* bufs = sm;                                               // 2 x [rows_in][Wt]
-  uint16_t* codes = reinterpret_cast<uint16_t*>(bufs + 2 * belems);  // [rows_out][cols]
-  unsigned* bins = reinterpret_cast<unsigned*>(codes + ((rows_out * cols + 1) & ~1));  // [nwarps][words]
+  float* bufs = sm;                                                // 2 x [rows_in][Wt]
+  unsigned* bins = reinterpret_cast<unsigned*>(bufs + 2 * belems);  // [br][nbx][words]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int w = threadIdx.x; w < A.br * A.nbx * words; w += CC_THREADS) bins[w] = 0u;
   cc_init_bars(A, bars);
   int64_t t = blockIdx.x;
   if (t < total) cc_issue(A, &tmap, &bars[0], SH, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
@@ -259,68 +261,51 @@ __global__ void __launch_bounds__(CC_THREADS)
     const int64_t m = t / bands;
     const int by0 = (int)(t % bands) * A.br;
     const int nbr = min(A.br, A.nby - by0);      // block rows in this band
-    // 1) codes of the band into shared memory
+    // 1) responses -> codes -> bins of the pixel's block
     const int band_rows = nbr * A.bh;
     for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += CC_THREADS) {
       const int r = s / G * PY, v0 = (s % G) * PX;
       float acc[PY][PX][NF];
       cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
+      const int bx0 = v0 / A.bw, rem0 = v0 - bx0 * A.bw;
 #pragma unroll
       for (int y = 0; y < PY; ++y)
         if (r + y < band_rows) {
-          if (PX % 4 == 0 && v0 + PX <= cols && (cols & 3) == 0) {
+          unsigned* rbins = bins + (r + y) / A.bh * A.nbx * words;
+          int bx = bx0, rem = rem0;
 #pragma unroll
-            for (int j4 = 0; j4 < PX / 4; ++j4) {
-              uint2 w;
-              w.x = cc_code<NF, PX, PY>(acc, y, 4 * j4, A.count) | cc_code<NF, PX, PY>(acc, y, 4 * j4 + 1, A.count) << 16;
-              w.y = cc_code<NF, PX, PY>(acc, y, 4 * j4 + 2, A.count) |
-                    cc_code<NF, PX, PY>(acc, y, 4 * j4 + 3, A.count) << 16;
-              *reinterpret_cast<uint2*>(codes + (r + y) * cols + v0 + 4 * j4) = w;
+          for (int j = 0; j < PX; ++j) {
+            if (v0 + j < cols) {
+              const unsigned code = cc_code<NF, PX, PY>(acc, y, j, A.count);
+              atomicAdd(&rbins[bx * words + (code >> 1)], 1u << ((code & 1u) << 4));
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < PX; ++j)
-              if (v0 + j < cols) codes[(r + y) * cols + v0 + j] = (uint16_t)cc_code<NF, PX, PY>(acc, y, j, A.count);
+            if (++rem == A.bw) {
+              rem = 0;
+              ++bx;
+            }
           }
         }
     }
     __syncthreads();
-    // 2) one warp per block: warp-private bins, counts out
-    unsigned* wb = bins + warp * words;
+    // 2) one warp per block: counts out, bins cleared for the next tile
     for (int blk = warp; blk < nbr * A.nbx; blk += nwarps) {
-      const int rb = blk / A.nbx, bx = blk % A.nbx;
-      for (int w = lane; w < words; w += 32) wb[w] = 0u;
-      __syncwarp();
-      const uint16_t* cb = codes + rb * A.bh * cols + bx * A.bw;
-      if (A.bw <= 32) {
-        // lanes tile (32 / bw) rows x bw columns per step
-        const int per = 32 / A.bw, lr = lane / A.bw, lc = lane - lr * A.bw;
-        if (lr < per)
-          for (int r = lr; r < A.bh; r += per) {
-            const unsigned code = cb[r * cols + lc];
-            atomicAdd(&wb[code >> 1], 1u << ((code & 1u) * 16));
-          }
-      } else {
-        for (int r = 0; r < A.bh; ++r)
-          for (int c = lane; c < A.bw; c += 32) {
-            const unsigned code = cb[r * cols + c];
-            atomicAdd(&wb[code >> 1], 1u << ((code & 1u) * 16));
-          }
-      }
-      __syncwarp();
+      const int rb = blk / A.nbx, bx = blk - rb * A.nbx;
+      unsigned* wb = bins + blk * words;
       const int64_t blk_global = (int64_t)(by0 + rb) * A.nbx + bx;
       const int64_t base = (m / A.gpr) * A.row_stride + (m % A.gpr) * A.group_stride + blk_global * nbins;
       if (A.kind == 2) {
         uint16_t* o = static_cast<uint16_t*>(A.counts) + base;
         for (int b = lane; b < nbins; b += 32) o[b] = (uint16_t)((wb[b >> 1] >> ((b & 1) * 16)) & 0xffffu);
       } else if ((nbins & 7) == 0) {
-        // 8 bins per lane per store
+        // 8 bins (4 words) per lane per store
         uint8_t* o = static_cast<uint8_t*>(A.counts) + base;
         for (int b8 = lane * 8; b8 < nbins; b8 += 256) {
+          const uint4 wv = *reinterpret_cast<const uint4*>(wb + (b8 >> 1));
+          const unsigned ww[4] = {wv.x, wv.y, wv.z, wv.w};
           uint32_t lo = 0, hi = 0;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            unsigned c = (wb[(b8 + k) >> 1] >> (((b8 + k) & 1) * 16)) & 0xffffu;
+            unsigned c = (ww[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
             c = c > 255u ? 255u : c;
             if (k < 4) lo |= c << (8 * k);
             else hi |= c << (8 * (k - 4));
@@ -335,6 +320,7 @@ __global__ void __launch_bounds__(CC_THREADS)
         }
       }
       __syncwarp();
+      for (int w = lane; w < words; w += 32) wb[w] = 0u;
     }
     __syncthreads();
   }
@@ -417,8 +403,7 @@ static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
   if (SH == 0) cc_tma_map(A, SH, Wt, rows_in, &tm);
   const int nbins = 1 << A.nbits;
   const size_t smem = sizeof(float) * 2 * (size_t)cc_buf_elems(rows_in, Wt) +
-                      sizeof(uint16_t) * (((size_t)rows_out * cols + 1) & ~1ull) +
-                      sizeof(unsigned) * (CC_THREADS / 32) * (size_t)((nbins + 1) / 2);
+                      sizeof(unsigned) * (size_t)A.br * A.nbx * (size_t)((nbins + 1) / 2);
   if (smem > 220 * 1024) return fail(DDCCA_ECONFIG, "conv_hist: band does not fit shared memory");
   const int64_t tiles = A.n_maps * ((A.nby + A.br - 1) / A.br);
   auto kern = conv_hist_kernel<L1, L2, NF, PX, PY, SH>;

@@ -322,6 +322,8 @@ class Engine:
             acc = self.work.setdefault(name, {"kind": work.get("kind"), "flops": 0.0, "bytes": 0.0, "calls": 0})
             acc["flops"] += work.get("flops", 0.0)
             acc["bytes"] += work.get("bytes", 0.0)
+            if "gram_flops" in work:
+                acc["gram_flops"] = acc.get("gram_flops", 0.0) + work["gram_flops"]
             acc["calls"] += 1
         if self.profile is None:
             return fn(*a, **k)
@@ -413,10 +415,14 @@ class Engine:
             mlab = labels[s0:s1].repeat_interleave(n_in) if n_in > 1 else labels[s0:s1]
             offs = np.cumsum([0] + [len(r) * n_in for r in group], dtype=np.int64)
             nmaps = int(offs[-1])
-            top, bottom, left, right = geom.pad_amounts(p, q)
-            ndx = -(-(2 * geom.l2 - 1) // 3) * 3
-            fl = 2.0 * 2 * nmaps * (p + top + bottom) * (q + left + right) * geom.l1 * ndx
-            self._timed(f"moments_l{len(layers) + 1}", 5, {"kind": "fp64", "flops": fl, "bytes": 8.0 * nmaps * p * q},
+            # algorithmic work: one DFMA per (own pixel, canonical lag), both views; the
+            # full-GEMM convention of the same statistics (2 d^2 per patch) as "gram_flops"
+            lags = geom.l1 * (2 * geom.l2 - 1) - (geom.l2 - 1)
+            fl = 2.0 * 2 * nmaps * p * q * lags
+            oh, ow = geom.out_shape(p, q)
+            gfl = 2.0 * 2 * nmaps * oh * ow * geom.dim * geom.dim
+            self._timed(f"moments_l{len(layers) + 1}", 5, {"kind": "fp64", "flops": fl, "gram_flops": gfl,
+                                                          "bytes": 8.0 * nmaps * p * q},
                         moments_partials, ex, m1, m2, mlab, offs, geom, center, classes,
                         out=parts[row:row + len(group)])
             row += len(group)
