@@ -356,6 +356,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "frac_of_3xtf32_ceiling": ach / (tf32 / 3.0),
                 "note": "exact FP64 lag form (85 DFMA/pixel at 7x7) instead of a 3xTF32 Gram (2 d^2 = 4802 "
                         "flop/patch); TF32 dense peak = measured bf16 / 2"}
+    if roof is not None:
+        # DRAM bytes per launch of the same kernel from the committed ncu launch list
+        tf = ROOT / "profiles" / "traffic.json"
+        kname = {"conv_hist": "conv_hist_kernel", "conv_l1": "conv_c_kernel", "conv_l2": "conv_c_kernel"}.get(
+            roof["kernel"], "lag_tma_kernel" if roof["kernel"].startswith("moments") else roof["kernel"])
+        if tf.exists():
+            t = json.loads(tf.read_text())
+            k = t.get("kernels", {}).get(kname)
+            if k:
+                roof["traffic"] = k["dram_bytes_per_launch"]
+                roof["traffic_unit"] = "bytes/launch (dram read+write)"
+                roof["traffic_source"] = "profiles/traffic.json: " + t.get("source", "")
+                w = kern[roof["kernel"]]["work"] or {}
+                if w.get("bytes"):
+                    roof["algorithmic_bytes"] = w["bytes"]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1

@@ -202,6 +202,25 @@ DDCCA_API int ddcca_iq_expand(const void* counts, int count_kind, int64_t n_bloc
 DDCCA_API int ddcca_im2col(const double* maps, int64_t n_maps, const ddcca_geom* g, int center, double* out,
                  void* stream);
 
+
+/* ---------------------------------------------------------------------
+ * Downstream nearest-neighbour classifier (classify.py:109-143):
+ * pred[i] = label of the training row nearest to query row i, squared
+ * euclidean (metric 0, q2 + t2 - 2 q.t, classify.py:113-115) or cosine
+ * (metric 1, classify.py:116-120); ties -> lowest label (classify.py:136-138).
+ * Rows: row_kind 3 = float64 features; 0 / 2 = u8 / u16 block counts expanded
+ * through `lut` (lut_len = bpc + 1 values, the iq LUT) while staged.
+ * Saturating-u8 counts go through ddcca_counts_to_u16 first.
+ * ------------------------------------------------------------------- */
+DDCCA_API size_t ddcca_nn_workspace(int64_t n_query, int64_t n_train);
+DDCCA_API int ddcca_nn_classify(const void* query, int64_t n_query, const void* train, int64_t n_train,
+                                int64_t dim, int row_kind, const double* lut, int lut_len,
+                                const int64_t* train_labels, int metric, int64_t* pred, void* workspace,
+                                size_t ws_bytes, void* stream);
+/* Saturating-u8 block counts (count_kind 1) -> exact u16 counts. */
+DDCCA_API int ddcca_counts_to_u16(const uint8_t* counts, int64_t n_blocks, int bins, int bpc, uint16_t* out,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

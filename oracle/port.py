@@ -25,7 +25,7 @@ __all__ = [
     "conv_stack", "conv_plane", "layer_stats", "train", "forward_maps",
     "EncodeCfg", "block_origins", "sign_bits", "combine_bits", "block_iq",
     "encode_maps", "encode_pair", "feature_len", "features", "Pool",
-    "iq_lut", "block_counts",
+    "iq_lut", "block_counts", "nn_predict", "nn_accuracy",
 ]
 
 
@@ -687,3 +687,37 @@ def features(view1, view2, layers, cfg: EncodeCfg, batch: int = 128, pool: Pool 
         return np.stack([encode_pair(m1[i], m2[i], n_bits, cfg)[0] for i in range(m1.shape[0])])
 
     return np.vstack(pool.map(run, batch_ranges(v1.shape[0], batch)))
+
+
+# ---------------------------------------------------------------------------
+# downstream nearest-neighbour classifier (classify.py:109-143)
+# ---------------------------------------------------------------------------
+
+def nn_predict(train: np.ndarray, labels: np.ndarray, queries: np.ndarray, metric: str = "euclidean",
+               chunk: int = 256) -> np.ndarray:
+    """Nearest training row per query; ties -> lowest label (classify.py:136-138).
+
+    euclidean: q2 + t2 - 2 q.t (classify.py:113-115); cosine: 1 - q.t / (|q||t|)
+    with similarity 0 where a norm is 0 (classify.py:116-120).
+    """
+    train = np.asarray(train, dtype=np.float64)
+    queries = np.asarray(queries, dtype=np.float64)
+    labels = np.asarray(labels, dtype=np.int64)
+    out = np.empty(queries.shape[0], dtype=np.int64)
+    for s in range(0, queries.shape[0], chunk):
+        q = queries[s:s + chunk]
+        dot = q @ train.T
+        if metric == "euclidean":
+            d = np.sum(q * q, axis=1)[:, None] + np.sum(train * train, axis=1)[None, :] - 2.0 * dot
+        else:
+            den = np.linalg.norm(q, axis=1)[:, None] * np.linalg.norm(train, axis=1)[None, :]
+            sim = np.divide(dot, den, out=np.zeros_like(dot), where=den > 0)
+            d = 1.0 - sim
+        for i, row in enumerate(d):
+            out[s + i] = labels[row == row.min()].min()
+    return out
+
+
+def nn_accuracy(pred: np.ndarray, labels: np.ndarray) -> float:
+    """evaluate (classify.py:150-176): trace(confusion) / n."""
+    return float(np.mean(np.asarray(pred) == np.asarray(labels)))

@@ -185,8 +185,39 @@ def main():
     v1 = f32(imgs)
     v2 = f32(np.stack([dd.lbp_map(im) for im in v1]))
     run_pipeline("pipeline_orl_mini", v1, v2, labels, 4, [(4, 5, 5), (4, 5, 5)], 16, 7, 7)
+    make_classify(dd)
     print("golden fixtures written to", OUT)
 
 
+def make_classify(dd):
+    """Reference NN classifier (classify.py:69-143) on pipeline features and on tie-heavy rows."""
+    from ddccanet import classify as C
+
+    rec = {}
+    orl = np.load(OUT / "pipeline_orl_mini.npz")
+    feats, labels = orl["features"], orl["labels"].astype(np.int64)
+    idx = np.arange(len(labels))
+    tr, te = idx[(idx // 4) % 2 == 0], idx[(idx // 4) % 2 == 1]  # every class on both sides
+    rec["orl_train"], rec["orl_test"] = tr, te
+    for metric in ("euclidean", "cosine"):
+        model = C.fit(feats[tr], labels[tr], kind="nearest_neighbor", metric=metric)
+        rec[f"orl_pred_{metric}"] = C.predict_many(model, feats[te])
+        rec[f"orl_acc_{metric}"] = C.evaluate(model, feats[te], labels[te]).accuracy
+    # duplicated integer rows under different labels: exact distance ties -> lowest label
+    rng = np.random.default_rng(5)
+    base = rng.integers(0, 4, size=(12, 9)).astype(np.float64)
+    train = np.concatenate([base, base[::-1], base[:5]])
+    tlab = np.concatenate([np.arange(12) % 5, (np.arange(12) + 2) % 5, np.arange(5)[::-1]]).astype(np.int64)
+    queries = np.concatenate([base + rng.integers(-1, 2, size=base.shape), np.zeros((2, 9)), base[:3]])
+    rec["tie_train"], rec["tie_labels"], rec["tie_queries"] = train, tlab, queries
+    for metric in ("euclidean", "cosine"):
+        model = C.fit(train, tlab, kind="nearest_neighbor", metric=metric)
+        rec[f"tie_pred_{metric}"] = C.predict_many(model, queries)
+    np.savez_compressed(OUT / "classify.npz", **rec)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["classify"]:
+        make_classify(_import_reference())
+    else:
+        main()

@@ -210,3 +210,18 @@ def test_pipeline_golden(golden, name):
     feats = O.features(g["v1"], g["v2"], layers, O.EncodeCfg(bh, bw), batch=int(g["batch"]))
     assert feats.shape == g["features"].shape
     assert np.mean(feats == g["features"]) >= 0.999
+
+
+# ---------------------------------------------------------------- classifier
+
+@pytest.mark.parametrize("metric", ["euclidean", "cosine"])
+def test_nn_classifier_golden(golden, metric):
+    """oracle.nn_predict == the reference's classify.fit/predict_many (incl. exact-tie rows)."""
+    g = golden("classify")
+    orl = golden("pipeline_orl_mini")
+    tr, te = g["orl_train"], g["orl_test"]
+    pred = O.nn_predict(orl["features"][tr], orl["labels"][tr], orl["features"][te], metric)
+    assert np.array_equal(pred, g[f"orl_pred_{metric}"])
+    assert O.nn_accuracy(pred, orl["labels"][te]) == float(g[f"orl_acc_{metric}"])
+    tie = O.nn_predict(g["tie_train"], g["tie_labels"], g["tie_queries"], metric)
+    assert np.array_equal(tie, g[f"tie_pred_{metric}"])
