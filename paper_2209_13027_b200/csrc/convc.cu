@@ -24,6 +24,10 @@
 namespace ddcca {
 
 constexpr int CC_THREADS = 256;
+// FFMAs per strip up to which the tap-row loop is unrolled. 0: always rolled. (Unrolling
+// does not turn the taps into immediate constant operands on sm_100a: the compiler
+// still stages them through uniform registers, at more LDCU per FFMA for short strips.)
+constexpr int CC_FULL_UNROLL = 0;
 
 template <int N>
 struct alignas(16) Taps {
@@ -70,10 +74,7 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
     for (int j = 0; j < PX; ++j)
 #pragma unroll
       for (int g = 0; g < NF; ++g) acc[y][j][g] = 0.f;
-  // rows stay rolled (keeps the loop body inside the instruction cache); taps of a
-  // row are warp-uniform constant-bank loads feeding the FFMAs
-#pragma unroll 1
-  for (int a = 0; a < L1 + PY - 1; ++a) {
+  auto row_step = [&](int a) {
     const float* row = tile + (r0 + a) * Wt + v0;
     constexpr int NX = PX + L2 - 1;
     constexpr int N4 = (NX + SH + 3) / 4;
@@ -102,6 +103,16 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
               acc[y][j][g] = fmaf(T.w[(ta * L2 + b) * NF + g], x[j + b], acc[y][j][g]);
       }
     }
+  };
+  if constexpr (L1 * L2 * NF * PX * PY <= CC_FULL_UNROLL) {
+    // small bodies: every tap is an immediate constant-bank operand of its FFMA
+#pragma unroll
+    for (int a = 0; a < L1 + PY - 1; ++a) row_step(a);
+  } else {
+    // large bodies stay rolled over rows (inside the instruction cache); the taps of
+    // a row are warp-uniform constant-bank loads feeding the FFMAs
+#pragma unroll 1
+    for (int a = 0; a < L1 + PY - 1; ++a) row_step(a);
   }
 }
 
@@ -429,6 +440,7 @@ static int run_shape(const CArgs& A, const float* pack_host, cudaStream_t st) {
 // Dispatch over the compiled (window, filter-count) shapes; DDCCA_ECONFIG = not covered.
 template <bool HIST>
 static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cudaStream_t st) {
+
 #define DDCCA_CC(L, NFV, PXV, PYV) \
   if (l1 == L && l2 == L && A.count <= NFV) return run_shape<HIST, L, NFV, PXV, PYV>(A, pack_host, st);
   DDCCA_CC(3, 8, 8, 1)

@@ -17,14 +17,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase
+// completes (or the hint expires) instead of spinning and stealing issue slots.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, unsigned parity) {
   unsigned done;
   asm volatile(
       "{\n.reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
       "selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(done)
-      : "r"(smem_u32(b)), "r"(parity)
+      : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
       : "memory");
   return done != 0;
 }
