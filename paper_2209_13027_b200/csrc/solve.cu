@@ -372,7 +372,80 @@ struct SolveArgs {
   int32_t* status;
   double* ws;  // global scratch
   int jacobi_in_smem;
+  int prewhitened;  // R1, R2 already computed by whiten_kernel (status checked first)
 };
+
+// Global scratch of one solve: [main Jacobi a/va (if not in smem)] [jtmp] R1 R2 T Gm U V NB ev
+// lam wsc sig flip lam2, then per whitening CTA b in {0,1}: [a/va] jtmp ev lam wsc.
+struct SolveLayout {
+  double *ja, *jva, *jtmp, *R1, *R2, *T, *Gm, *U, *V, *NB, *ev, *lam, *wsc, *sig, *flip, *lam2;
+  double* side;  // start of the whitening CTAs' scratch
+};
+
+__device__ __forceinline__ SolveLayout solve_layout(double* g, int n, bool in_smem, double* smem_base) {
+  const int nn = n * n;
+  SolveLayout L;
+  if (in_smem) {
+    L.ja = smem_base;
+    L.jva = smem_base + nn;
+  } else {
+    L.ja = g;
+    L.jva = g + nn;
+  }
+  g += 2 * nn;  // reserved either way so the layout does not depend on in_smem
+  L.jtmp = g; g += nn;
+  L.R1 = g; g += nn;
+  L.R2 = g; g += nn;
+  L.T = g; g += nn;
+  L.Gm = g; g += nn;
+  L.U = g; g += nn;
+  L.V = g; g += nn;   // right vectors (n x L used)
+  L.NB = g; g += nn;  // null basis
+  L.ev = g; g += nn;  // eigvec scratch
+  L.lam = g; g += n;
+  L.wsc = g; g += 2 * n + 2;
+  L.sig = g; g += n;
+  L.flip = g; g += n;
+  L.lam2 = g; g += n;
+  L.side = g;
+  return L;
+}
+__host__ __device__ inline size_t solve_side_doubles(int n) { return 4 * (size_t)n * n + 3 * (size_t)n + 2; }
+
+// Whitening (solver.py:227-229) of both views in parallel: CTA b computes
+// inv_sqrt(C_bb) into R1 / R2 with its own Jacobi scratch.
+__global__ void __launch_bounds__(SOLVE_THREADS) whiten_kernel(SolveArgs S) {
+  extern __shared__ double sm[];
+  __shared__ double red[SOLVE_THREADS / 32 + 1];
+  __shared__ int flag;
+  if (*S.status != 0) return;  // finalize failed
+  const int n = S.d, nn = n * n;
+  const int b = blockIdx.x;
+  int* iscr = reinterpret_cast<int*>(sm);
+  double* cs = sm + (2 * n + 2 + 1) / 2 + 1;
+  double* base = cs + 2 * n + 2;
+  SolveLayout L = solve_layout(S.ws, n, false, nullptr);
+  double* g = L.side + (size_t)b * solve_side_doubles(n);
+  double *ja, *jva;
+  if (S.jacobi_in_smem) {
+    ja = base;
+    jva = base + nn;
+  } else {
+    ja = g;
+    jva = g + nn;
+  }
+  g += 2 * nn;
+  double* jtmp = g; g += nn;
+  double* ev = g; g += nn;
+  double* lam = g; g += n;
+  double* wsc = g;
+  if (threadIdx.x == 0) flag = 0;
+  __syncthreads();
+  Blk B{red, &flag, iscr};
+  const double* c = S.fin + (b == 0 ? 0 : nn);
+  const int rc = inv_sqrt_dev(c, n, b == 0 ? L.R1 : L.R2, lam, ev, ja, jva, cs, jtmp, wsc, B);
+  if (rc != DDCCA_OK && threadIdx.x == 0) atomicCAS(reinterpret_cast<int*>(S.status), 0, rc);
+}
 
 __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
   extern __shared__ double sm[];
@@ -380,50 +453,36 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
   __shared__ int flag;
   const int n = S.d, C = S.C, L = S.count;
   const int nn = n * n;
+  if (S.prewhitened && *S.status != 0) return;
   int* iscr = reinterpret_cast<int*>(sm);  // 2n+2 ints
   double* cs = sm + (2 * n + 2 + 1) / 2 + 1;  // 2n+2 doubles: per-round rotations
   double* base = cs + 2 * n + 2;
-  double *ja, *jva;
-  double* g = S.ws;
-  if (S.jacobi_in_smem) {
-    ja = base;
-    jva = base + nn;
-  } else {
-    ja = g;
-    jva = g + nn;
-    g += 2 * nn;
-  }
-  double* jtmp = g; g += nn;
+  const SolveLayout Y = solve_layout(S.ws, n, S.jacobi_in_smem != 0, base);
+  double *ja = Y.ja, *jva = Y.jva, *jtmp = Y.jtmp, *R1 = Y.R1, *R2 = Y.R2, *T = Y.T, *Gm = Y.Gm, *U = Y.U,
+         *V = Y.V, *NB = Y.NB, *ev = Y.ev, *lam = Y.lam, *wsc = Y.wsc, *sig = Y.sig, *flip = Y.flip,
+         *lam2 = Y.lam2;
   Blk B{red, &flag, iscr};
-  double* c11 = S.fin;
-  double* c22 = S.fin + nn;
   double* ct = S.fin + 4 * nn;
-  double* R1 = g; g += nn;
-  double* R2 = g; g += nn;
-  double* T = g; g += nn;
-  double* Gm = g; g += nn;
-  double* U = g; g += nn;
-  double* V = g; g += nn;   // right vectors (n x L used)
-  double* NB = g; g += nn;  // null basis
-  double* ev = g; g += nn;  // eigvec scratch
-  double* lam = g; g += n;
-  double* wsc = g; g += 2 * n + 2;
-  double* sig = g; g += n;
-  double* flip = g; g += n;
-  double* lam2 = g; g += n;
-  if (threadIdx.x == 0) { flag = 0; *S.status = 0; }
+  if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  // ---- finalize (moments.py:168-193); payload == nullptr: fin already holds finalized moments
-  if (S.payload != nullptr && !finalize_dev(S.payload, n, C, S.eps, S.fin, B)) {
-    if (threadIdx.x == 0) *S.status = DDCCA_ENUMERICAL;
-    return;
-  }
-  // ---- whitening (solver.py:227-229)
-  int rc = inv_sqrt_dev(c11, n, R1, lam, ev, ja, jva, cs, jtmp, wsc, B);
-  if (rc == DDCCA_OK) rc = inv_sqrt_dev(c22, n, R2, lam, ev, ja, jva, cs, jtmp, wsc, B);
-  if (rc != DDCCA_OK) {
-    if (threadIdx.x == 0) *S.status = rc;
-    return;
+  int rc = DDCCA_OK;
+  if (!S.prewhitened) {
+    double* c11 = S.fin;
+    double* c22 = S.fin + nn;
+    if (threadIdx.x == 0) *S.status = 0;
+    __syncthreads();
+    // ---- finalize (moments.py:168-193); payload == nullptr: fin already holds finalized moments
+    if (S.payload != nullptr && !finalize_dev(S.payload, n, C, S.eps, S.fin, B)) {
+      if (threadIdx.x == 0) *S.status = DDCCA_ENUMERICAL;
+      return;
+    }
+    // ---- whitening (solver.py:227-229)
+    rc = inv_sqrt_dev(c11, n, R1, lam, ev, ja, jva, cs, jtmp, wsc, B);
+    if (rc == DDCCA_OK) rc = inv_sqrt_dev(c22, n, R2, lam, ev, ja, jva, cs, jtmp, wsc, B);
+    if (rc != DDCCA_OK) {
+      if (threadIdx.x == 0) *S.status = rc;
+      return;
+    }
   }
   matmul(R1, false, ct, false, Gm, n, n, n);  // Gm = R1 ct
   matmul(Gm, false, R2, false, T, n, n, n);   // T = R1 ct R2
@@ -591,7 +650,7 @@ extern "C" {
 
 size_t ddcca_solve_workspace(int dim) {
   const size_t nn = (size_t)dim * dim;
-  return sizeof(double) * (14 * nn + 8 * (size_t)dim + 16);
+  return sizeof(double) * (14 * nn + 8 * (size_t)dim + 16 + 2 * solve_side_doubles(dim));
 }
 
 int ddcca_solve(const double* payload, int dim, int class_count, double epsilon, int count, double* fin, double* w1,
@@ -606,9 +665,18 @@ int ddcca_solve(const double* payload, int dim, int class_count, double epsilon,
   const bool in_smem = dim <= SMEM_JACOBI_MAX_N;
   const size_t sm = jacobi_smem(dim, in_smem);
   SolveArgs S{payload, dim, class_count, count, epsilon, fin, w1, w2, rho, conv_pack1, conv_pack2, status,
-              static_cast<double*>(ws), in_smem ? 1 : 0};
+              static_cast<double*>(ws), in_smem ? 1 : 0, 1};
+  cudaStream_t st = as_stream(stream);
+  // finalize -> both whitenings in parallel (two CTAs) -> T, eig(T T^T), filters
+  if (payload != nullptr) {
+    finalize_kernel<<<1, SOLVE_THREADS, 0, st>>>(payload, dim, class_count, epsilon, fin, status);
+  } else {
+    cudaMemsetAsync(status, 0, sizeof(int32_t), st);
+  }
+  cudaFuncSetAttribute(whiten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  whiten_kernel<<<2, SOLVE_THREADS, sm, st>>>(S);
   cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  solve_kernel<<<1, SOLVE_THREADS, sm, as_stream(stream)>>>(S);
+  solve_kernel<<<1, SOLVE_THREADS, sm, st>>>(S);
   return check_launch("solve_kernel");
 }
 

@@ -478,7 +478,7 @@ class Engine:
                 parts = self.layer_partials(images1, images2, labels, layers, cfg.geom, cfg.center, classes, local,
                                             first_sample, keep=last and self.keep_maps_bytes > 0)
                 merged = self.reduce_partials(parts, len(gb), mine)
-                layer = self._timed(f"solve_l{i + 1}", 1, None, solve_layer, ex, merged, cfg.geom, cfg.filters,
+                layer = self._timed(f"solve_l{i + 1}", 3, None, solve_layer, ex, merged, cfg.geom, cfg.filters,
                                     cfg.center, classes, eps)
                 layers.append(layer)
                 if keep_stats:
