@@ -16,7 +16,18 @@
 
 namespace ddcca {
 
-constexpr int SOLVE_THREADS = 256;
+constexpr int SOLVE_THREADS = 512;  // latency-bound rounds: more warps per rotation pass
+
+#ifdef DDCCA_SOLVE_PROF  // diagnostic build only (tools/microbench/jacobi_probe.cu)
+__device__ unsigned long long g_solve_prof[8];
+#define PROF_MARK(t) const long long t = clock64()
+#define PROF_ADD(k, t0) do { if (threadIdx.x == 0) g_solve_prof[k] += clock64() - (t0); } while (0)
+#define PROF_COUNT_SWEEP() do { if (threadIdx.x == 0) g_solve_prof[7] += 1; } while (0)
+#else
+#define PROF_MARK(t)
+#define PROF_ADD(k, t0)
+#define PROF_COUNT_SWEEP()
+#endif
 constexpr int SMEM_JACOBI_MAX_N = 110;  // 2*n*n doubles in shared memory
 
 struct Blk {
@@ -162,9 +173,14 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
   int* pp = B.iscr;          // p of pair t
   int* qq = B.iscr + npair;  // q of pair t (or -1 if inactive / dummy)
   bool converged = false;
+  PROF_MARK(t_start);
   for (int sweep = 0; sweep < 100; ++sweep) {
+    PROF_MARK(t_off);
     if (offdiag_norm(a, n, B) <= 1e-12) { converged = true; break; }
+    PROF_ADD(0, t_off);
+    PROF_COUNT_SWEEP();
     for (int r = 0; r < m - 1; ++r) {
+      PROF_MARK(t_round);
       for (int t = threadIdx.x; t < npair; t += blockDim.x) {
         const int u = rr_seat(t, r, m), x = rr_seat(m - 1 - t, r, m);
         int p = min(u, x), q = max(u, x);
@@ -172,10 +188,15 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
         if (q < n) {
           const double apq = a[p * n + q];
           if (apq != 0.0) {
-            const double theta = (a[q * n + q] - a[p * n + p]) / (2.0 * apq);
-            const double sg = theta >= 0.0 ? 1.0 : -1.0;
-            const double tt = sg / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(tt * tt + 1.0);
+            // theta = (a_qq - a_pp) / (2 a_pq), t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)),
+            // c = 1 / sqrt(t^2 + 1), s = t c (solver.py:32-46), with numerator and denominator
+            // of t scaled by |2 a_pq|: one division, one sqrt and one rsqrt on the round's
+            // critical path instead of three divisions and two square roots.
+            const double dlt = a[q * n + q] - a[p * n + p];
+            const double two = 2.0 * apq;
+            const double sg = ((dlt >= 0.0) == (two > 0.0)) || dlt == 0.0 ? 1.0 : -1.0;
+            const double tt = sg * fabs(two) / (fabs(dlt) + sqrt(fma(dlt, dlt, two * two)));
+            c = rsqrt(fma(tt, tt, 1.0));
             sn = tt * c;
           } else {
             q = -1;
@@ -189,6 +210,8 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
         cs[2 * t + 1] = sn;
       }
       __syncthreads();
+      PROF_ADD(1, t_round);
+      PROF_MARK(t_upd);
       // rows: B = J^T a   (warp per pair, lanes over columns)
       for (int t = warp; t < npair; t += nwarps) {
         const int q = qq[t];
@@ -218,6 +241,7 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
         }
       }
       __syncthreads();
+      PROF_ADD(2, t_upd);
     }
     // a = (a + a^T) / 2
     for (int e = threadIdx.x; e < nn; e += blockDim.x) {
@@ -230,6 +254,8 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
     }
     __syncthreads();
   }
+  PROF_ADD(3, t_start);
+  PROF_MARK(t_post);
   if (!converged && offdiag_norm(a, n, B) > 1e-12) return DDCCA_ENUMERICAL;
   // eigenvalues, stable descending order
   for (int i = threadIdx.x; i < n; i += blockDim.x) wtmp[i] = a[i * n + i] * norm;
@@ -275,6 +301,7 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = wtmp[i];
   __syncthreads();
+  PROF_ADD(4, t_post);
   return DDCCA_OK;
 }
 
