@@ -139,7 +139,7 @@ __device__ __forceinline__ void cc_issue(const CArgs& A, const CUtensorMap* tm, 
     return;
   }
   const float* img = A.in + m * (int64_t)A.p * A.q;
-  for (int r = threadIdx.x >> 5; r < rows; r += CC_THREADS / 32) {
+  for (int r = threadIdx.x >> 5; r < rows; r += blockDim.x / 32) {
     const int i = row0 + r - A.top;
     const bool rok = i >= 0 && i < A.p;
     const float* rowp = img + (int64_t)i * A.q;
@@ -174,14 +174,14 @@ __device__ __forceinline__ void cc_init_bars(const CArgs& A, uint64_t* bars) {
 }
 
 // Persistent float-response conv (MODE 0): tiles = (map, band of rows_per_tile output rows).
-template <int L1, int L2, int NF, int PX, int PY, int SH>
-__global__ void __launch_bounds__(CC_THREADS)
+template <int L1, int L2, int NF, int PX, int PY, int SH, int NT>
+__global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     conv_c_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t bars[2];
   const int G = (A.ow + PX - 1) / PX;
   const int Wt = cc_tile_width(A.ow, L2, PX, SH);
-  const int rows_out = PY * max(1, CC_THREADS / G);  // output rows per tile (one strip per thread)
+  const int rows_out = PY * max(1, NT / G);  // output rows per tile (one strip per thread)
   const int rows_in = rows_out + L1 - 1;
   const int bands = (A.oh + rows_out - 1) / rows_out;
   const int64_t total = A.n_maps * bands;
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(CC_THREADS)
 // Fused last layer: sign codes of BR block-rows go straight into per-block shared
 // bins (packed u16 pairs, CTA-wide atomics); then one warp per block writes the
 // counts into the feature row and clears the bins.
-template <int L1, int L2, int NF, int PX, int PY, int SH>
-__global__ void __launch_bounds__(CC_THREADS)
+template <int L1, int L2, int NF, int PX, int PY, int SH, int NT>
+__global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t bars[2];
@@ -252,11 +252,11 @@ __global__ void __launch_bounds__(CC_THREADS)
   const int64_t total = A.n_maps * bands;
   const int nbins = 1 << A.nbits;
   const int words = (nbins + 1) / 2;
-  const int nwarps = CC_THREADS / 32;
+  const int nwarps = NT / 32;
   float* bufs = sm;                                                // 2 x [rows_in][Wt]
   unsigned* bins = reinterpret_cast<unsigned*>(bufs + 2 * belems);  // [br][nbx][words]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int w = threadIdx.x; w < A.br * A.nbx * words; w += CC_THREADS) bins[w] = 0u;
+  for (int w = threadIdx.x; w < A.br * A.nbx * words; w += NT) bins[w] = 0u;
   cc_init_bars(A, bars);
   int64_t t = blockIdx.x;
   if (t < total) cc_issue(A, &tmap, &bars[0], SH, t / bands, (int)(t % bands) * rows_out, rows_in, Wt, bufs);
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(CC_THREADS)
     const int nbr = min(A.br, A.nby - by0);      // block rows in this band
     // 1) responses -> codes -> bins of the pixel's block
     const int band_rows = nbr * A.bh;
-    for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += CC_THREADS) {
+    for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += NT) {
       const int r = s / G * PY, v0 = (s % G) * PX;
       float acc[PY][PX][NF];
       cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
@@ -353,13 +353,13 @@ static void zero_mean_taps(const float* pack_host, int count, int d, int nf, boo
 
 // Grid for a persistent kernel: resident CTAs per SM x SMs, capped by the tile count.
 template <typename K>
-static int persistent_grid(K kern, size_t smem, int64_t tiles) {
+static int persistent_grid(K kern, size_t smem, int64_t tiles, int threads = CC_THREADS) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CC_THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(1, per_sm) * sms));
   return (int)grid;
 }
@@ -378,13 +378,13 @@ static bool cc_tma_map(CArgs& A, int sh, int Wt, int rows_in, CUtensorMap* tm) {
   return A.use_tma != 0;
 }
 
-template <int L1, int L2, int NF, int PX, int PY, int SH>
+template <int L1, int L2, int NF, int PX, int PY, int SH, int NT = CC_THREADS>
 static int run_conv_c(CArgs A, const float* pack_host, cudaStream_t st) {
   Taps<L1 * L2 * NF> T;
   zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
   const int G = (A.ow + PX - 1) / PX;
   const int Wt = cc_tile_width(A.ow, L2, PX, SH);
-  const int rows_out = PY * std::max(1, CC_THREADS / G);
+  const int rows_out = PY * std::max(1, NT / G);
   const int rows_in = rows_out + L1 - 1;
   CUtensorMap tm;
   if (SH != 0 && !cc_tma_map(A, SH, Wt, rows_in, &tm)) return DDCCA_ECONFIG;  // caller retries with SH = 0
@@ -392,20 +392,20 @@ static int run_conv_c(CArgs A, const float* pack_host, cudaStream_t st) {
   const size_t smem = sizeof(float) * 2 * (size_t)cc_buf_elems(rows_in, Wt);
   if (smem > 200 * 1024) return fail(DDCCA_ECONFIG, "conv: map row too wide for shared-memory staging");
   const int64_t tiles = A.n_maps * ((A.oh + rows_out - 1) / rows_out);
-  auto kern = conv_c_kernel<L1, L2, NF, PX, PY, SH>;
-  const int grid = persistent_grid(kern, smem, tiles);
-  kern<<<grid, CC_THREADS, smem, st>>>(A, T, tm);
+  auto kern = conv_c_kernel<L1, L2, NF, PX, PY, SH, NT>;
+  const int grid = persistent_grid(kern, smem, tiles, NT);
+  kern<<<grid, NT, smem, st>>>(A, T, tm);
   return check_launch("conv_c_kernel");
 }
 
-template <int L1, int L2, int NF, int PX, int PY, int SH>
+template <int L1, int L2, int NF, int PX, int PY, int SH, int NT = CC_THREADS>
 static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
   Taps<L1 * L2 * NF> T;
   zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
   const int cols = A.nbx * A.bw;
   const int G = (cols + PX - 1) / PX;
   // block rows per CTA: about one strip per thread, at least one block row
-  A.br = std::max(1, std::min(A.nby, PY * CC_THREADS / std::max(1, A.bh * G)));
+  A.br = std::max(1, std::min(A.nby, PY * NT / std::max(1, A.bh * G)));
   const int rows_out = A.br * A.bh;
   const int Wt = cc_tile_width(cols, L2, PX, SH);
   const int rows_in = (rows_out + PY - 1) / PY * PY + L1 - 1;
@@ -417,30 +417,43 @@ static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
                       sizeof(unsigned) * (size_t)A.br * A.nbx * (size_t)((nbins + 1) / 2);
   if (smem > 220 * 1024) return fail(DDCCA_ECONFIG, "conv_hist: band does not fit shared memory");
   const int64_t tiles = A.n_maps * ((A.nby + A.br - 1) / A.br);
-  auto kern = conv_hist_kernel<L1, L2, NF, PX, PY, SH>;
-  const int grid = persistent_grid(kern, smem, tiles);
-  kern<<<grid, CC_THREADS, smem, st>>>(A, T, tm);
+  auto kern = conv_hist_kernel<L1, L2, NF, PX, PY, SH, NT>;
+  const int grid = persistent_grid(kern, smem, tiles, NT);
+  kern<<<grid, NT, smem, st>>>(A, T, tm);
   return check_launch("conv_hist_kernel");
 }
 
 // Column shift that 16 B aligns the TMA box origin -(left + sh) for "same" padding.
 constexpr int same_shift(int l2) { return (4 - ((l2 - 1) / 2) % 4) % 4; }
 
-template <bool HIST, int L, int NF, int PX, int PY>
+template <bool HIST, int L, int NF, int PX, int PY, int NT = CC_THREADS>
 static int run_shape(const CArgs& A, const float* pack_host, cudaStream_t st) {
   constexpr int S = same_shift(L);
   const int want = (4 - A.left % 4) % 4;
   if (S != 0 && want == S) {
-    const int rc = HIST ? run_conv_hist<L, L, NF, PX, PY, S>(A, pack_host, st) : run_conv_c<L, L, NF, PX, PY, S>(A, pack_host, st);
+    const int rc = HIST ? run_conv_hist<L, L, NF, PX, PY, S, NT>(A, pack_host, st)
+                        : run_conv_c<L, L, NF, PX, PY, S, NT>(A, pack_host, st);
     if (rc != DDCCA_ECONFIG) return rc;
   }
-  return HIST ? run_conv_hist<L, L, NF, PX, PY, 0>(A, pack_host, st) : run_conv_c<L, L, NF, PX, PY, 0>(A, pack_host, st);
+  return HIST ? run_conv_hist<L, L, NF, PX, PY, 0, NT>(A, pack_host, st)
+              : run_conv_c<L, L, NF, PX, PY, 0, NT>(A, pack_host, st);
 }
 
 // Dispatch over the compiled (window, filter-count) shapes; DDCCA_ECONFIG = not covered.
 template <bool HIST>
 static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cudaStream_t st) {
-
+  // 8 filters: 16-pixel strips in 128-thread CTAs (3 per SM) halve the tap loads per
+  // FFMA; DDCCA_CH8=1 selects the 8-pixel / 256-thread form (A/B)
+  const char* ch8 = getenv("DDCCA_CH8");
+  if (A.count <= 8 && !(ch8 && ch8[0] == '1')) {
+#define DDCCA_CH(L) \
+    if (l1 == L && l2 == L) return run_shape<HIST, L, 8, 16, 1, 128>(A, pack_host, st);
+    DDCCA_CH(3)
+    DDCCA_CH(5)
+    DDCCA_CH(7)
+    DDCCA_CH(9)
+#undef DDCCA_CH
+  }
 #define DDCCA_CC(L, NFV, PXV, PYV) \
   if (l1 == L && l2 == L && A.count <= NFV) return run_shape<HIST, L, NFV, PXV, PYV>(A, pack_host, st);
   DDCCA_CC(3, 8, 8, 1)
