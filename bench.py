@@ -285,8 +285,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         h2 = img2.cpu().pin_memory()
         hl = torch.from_numpy(lab.astype(np.int64))
         host_counts = torch.empty((s1 - s0, featlen), dtype=torch.int16 if kind == 2 else torch.uint8).pin_memory()
-        ds = P.ViewPairDataset.from_arrays(h1.numpy(), h2.numpy(), hl.numpy(), class_count=classes)
-        ds._stacks = (h1, h2, hl.numpy())
+        ds = P.ViewPairDataset.from_arrays(h1, h2, hl.numpy(), class_count=classes)  # pinned: chunked async upload
         net = P.NetworkConfig(tuple(layer_cfgs), batch=P.BatchSpec(bs))
         pcfg = type("Cfg", (), {"net": net, "encoder": enc})()
 

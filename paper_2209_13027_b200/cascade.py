@@ -239,8 +239,14 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
     s1 = gb[mine.stop - 1].stop if len(mine) else 0
     eng = E.Engine(ex)
     with torch.cuda.stream(ex.stream):
-        i1 = _to_dev32(ex, _rows(v1, s0, s1))
-        i2 = _to_dev32(ex, _rows(v2, s0, s1))
+        h1, h2 = _rows(v1, s0, s1), _rows(v2, s0, s1)
+        if _pinned(h1) and _pinned(h2):
+            # pinned host views: upload in chunks on a copy stream; the first layer's
+            # moments start on each chunk as it lands (Engine.upload_events)
+            i1, i2, eng.upload_events = _upload_chunked(ex, h1, h2, UPLOAD_CHUNK_BATCHES * bs)
+        else:
+            i1 = _to_dev32(ex, h1)
+            i2 = _to_dev32(ex, h2)
         ld = _labels_dev(ex, lab[s0:s1])
         res = eng.fit(i1, i2, ld, ds.class_count, list(cfg.layers), bs, cfg.epsilon, n_global=n, first_sample=s0,
                       stage_hook=stage_hook)
@@ -251,6 +257,42 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
     ds._device_state = {"device": str(ex.device), "rows": (s0, s1), "images": (i1, i2), "engine": eng,
                         "bank": id(bank)}
     return bank
+
+
+UPLOAD_CHUNK_BATCHES = 16  # sample batches per image upload chunk
+
+
+def _pinned(a) -> bool:
+    import torch
+
+    return isinstance(a, torch.Tensor) and a.dtype == torch.float32 and a.is_pinned() and a.is_contiguous()
+
+
+def _upload_chunked(ex, h1, h2, rows_per_chunk: int):
+    """Pinned (m, p, q) float32 views -> device tensors filled chunk by chunk on a side stream.
+
+    Returns (d1, d2, [(row_end, event)]); ex.stream must wait on a chunk's event
+    before reading its rows (Engine.layer_partials does).
+    """
+    import torch
+
+    m = h1.shape[0]
+    d1 = torch.empty(h1.shape, dtype=torch.float32, device=ex.device)
+    d2 = torch.empty(h2.shape, dtype=torch.float32, device=ex.device)
+    up = torch.cuda.Stream(device=ex.device)
+    up.wait_stream(ex.stream)  # the fresh buffers' memory may still be in use by earlier work
+    events = []
+    with torch.cuda.stream(up):
+        for r0 in range(0, m, max(1, rows_per_chunk)):
+            r1 = min(m, r0 + rows_per_chunk)
+            d1[r0:r1].copy_(h1[r0:r1], non_blocking=True)
+            d2[r0:r1].copy_(h2[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+            events.append((r1, ev))
+    d1.record_stream(up)
+    d2.record_stream(up)
+    return d1, d2, events
 
 
 def _rows(a, s0: int, s1: int):

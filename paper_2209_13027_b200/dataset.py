@@ -29,6 +29,11 @@ class ViewPairSample:
             raise ParseError(f"negative class label {self.label}")
 
 
+def _is_tensor(a) -> bool:
+    t = type(a)
+    return t.__module__.startswith("torch") and t.__name__ == "Tensor"
+
+
 @dataclass
 class ViewPairDataset:
     """Ordered labelled view pairs with contiguous class ids."""
@@ -40,8 +45,10 @@ class ViewPairDataset:
 
     @classmethod
     def from_arrays(cls, view1, view2, labels, class_count: int | None = None, label_map=None):
-        v1 = np.asarray(view1)
-        v2 = np.asarray(view2)
+        # pinned torch tensors are kept as they are: train_network then uploads them
+        # asynchronously, chunk by chunk, overlapped with the first layer's moments
+        v1 = view1 if _is_tensor(view1) else np.asarray(view1)
+        v2 = view2 if _is_tensor(view2) else np.asarray(view2)
         lab = np.asarray(labels, dtype=np.int64)
         if v1.ndim != 3 or v1.shape != v2.shape:
             raise ShapeError(f"need two equal (M, p, q) stacks, got {v1.shape} and {v2.shape}")

@@ -310,6 +310,7 @@ class Engine:
     def __init__(self, executor, map_budget_bytes: int = MAP_BUDGET_BYTES, keep_maps_bytes: int = KEEP_MAPS_BYTES):
         self.ex = executor
         self.budget = map_budget_bytes
+        self.upload_events = []  # [(local row end, cuda event)] of an in-flight chunked image upload
         self.keep_maps_bytes = keep_maps_bytes
         self.maps_cache = None  # last hidden layer's maps of the fitted shard, reused by the transform
         self.profile = None   # dict name -> [(start_event, end_event)] when profiling
@@ -375,6 +376,23 @@ class Engine:
         return groups
 
     @staticmethod
+    def _split_at(groups: list, ends: list, first_sample: int) -> list:
+        """Split batch groups so no group crosses an upload-chunk boundary (local row ``ends``)."""
+        out = []
+        for g in groups:
+            cur, cur_chunk = [], None
+            for r in g:
+                chunk = next(i for i, e in enumerate(ends) if e >= r.stop - first_sample)
+                if cur and chunk != cur_chunk:
+                    out.append(cur)
+                    cur = []
+                cur.append(r)
+                cur_chunk = chunk
+            if cur:
+                out.append(cur)
+        return out
+
+    @staticmethod
     def _maps_per_sample(layers: list) -> int:
         return int(np.prod([lay.count for lay in layers])) if layers else 1
 
@@ -404,8 +422,19 @@ class Engine:
             keep_buf = (torch.empty((m_local * n_in, p, q), dtype=torch.float32, device=ex.device),
                         torch.empty((m_local * n_in, p, q), dtype=torch.float32, device=ex.device))
         row = 0
-        for group in self._superbatches(batch_ranges, n_in * p * q * 4):
+        groups = self._superbatches(batch_ranges, n_in * p * q * 4)
+        uploads = self.upload_events if not layers else []
+        if uploads:
+            # images still arriving (train_network's chunked upload): one group per upload
+            # chunk, each waiting only for its own rows, so the copies overlap the moments
+            ends = [e for e, _ in uploads]
+            groups = self._split_at(groups, ends, first_sample)
+        for group in groups:
             s0, s1 = group[0].start - first_sample, group[-1].stop - first_sample
+            for end, ev in uploads:
+                if end >= s1:
+                    ex.stream.wait_event(ev)
+                    break
             if keep_buf is not None:
                 m1 = self._forward(images1[s0:s1], layers, 1, out=keep_buf[0][s0 * n_in:s1 * n_in])
                 m2 = self._forward(images2[s0:s1], layers, 2, out=keep_buf[1][s0 * n_in:s1 * n_in])
@@ -483,6 +512,7 @@ class Engine:
                 layers.append(layer)
                 if keep_stats:
                     stats.append(merged)
+        self.upload_events = []
         return FitResult(layers, stats)
 
     # -- transform ---------------------------------------------------------

@@ -403,3 +403,32 @@ def test_tma_moments_path_matches_oracle(ex, l, p, q, nm, monkeypatch):
     monkeypatch.setenv("DDCCA_NO_TMA", "1")
     alt = P.accumulate_layer_moments(out, geom, True, classes, P.BatchSpec(6), ex)
     assert rel(got.c11, alt.c11) <= 1e-13 and rel(got.c22, alt.c22) <= 1e-13
+
+
+def test_pinned_chunked_upload_same_bank(ex):
+    """Pinned host views take the chunked, overlapped upload; the bank equals the numpy-input bank bit for bit."""
+    from paper_2209_13027_b200 import cascade as Cc
+    from paper_2209_13027_b200 import synthetic as S
+
+    imgs, labels = S.blob_images(200, 20, 16, 5, seed=11)
+    v1 = imgs.astype(np.float32)
+    v2 = S.second_view(v1, labels, "channel", 5, seed=12).astype(np.float32)
+    net = P.NetworkConfig((P.LayerConfig(4, P.PatchGeometry(3, 3)), P.LayerConfig(4, P.PatchGeometry(3, 3))),
+                          batch=P.BatchSpec(16))
+    ds_np = P.ViewPairDataset.from_arrays(v1, v2, labels, class_count=5)
+    h1 = torch.from_numpy(v1).pin_memory()
+    h2 = torch.from_numpy(v2).pin_memory()
+    ds_pin = P.ViewPairDataset.from_arrays(h1, h2, labels, class_count=5)
+    old = Cc.UPLOAD_CHUNK_BATCHES
+    Cc.UPLOAD_CHUNK_BATCHES = 3  # several chunks, groups split at chunk ends
+    try:
+        b_pin = P.train_network(ds_pin, net, ex)
+    finally:
+        Cc.UPLOAD_CHUNK_BATCHES = old
+    b_np = P.train_network(ds_np, net, ex)
+    for a, b in zip(b_pin.layers, b_np.layers):
+        assert np.array_equal(a.filters1, b.filters1) and np.array_equal(a.filters2, b.filters2)
+    cfg = type("Cfg", (), {"net": net, "encoder": P.EncoderConfig(4, 4)})()
+    c_pin, _ = P.compute_feature_counts(ds_pin, b_pin, cfg, ex)
+    c_np, _ = P.compute_feature_counts(ds_np, b_np, cfg, ex)
+    assert torch.equal(c_pin, c_np)
