@@ -33,7 +33,7 @@ from .patches import PatchGeometry
 
 MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
 KEEP_MAPS_BYTES = 48 << 30  # fit keeps the last layer's input maps (both views) for the transform if they fit
-HOST_CHUNK_BATCHES = 12  # sample batches per streamed device->host count copy
+HOST_CHUNK_BATCHES = 4  # sample batches per streamed device->host count copy
 
 
 
