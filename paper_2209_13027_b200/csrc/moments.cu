@@ -644,6 +644,32 @@ __global__ void __launch_bounds__(RS_WARPS * 32) rect_sums_kernel(RectArgs A) {
     int ye = y;
     while (ye < A.Hp && A.rz_of_y[ye] == rz) ++ye;
     const int i0 = max(y - A.top, 0), i1 = min(ye - A.top, A.p);
+    if (vec && A.q <= 128) {
+      // one float4 per lane per row; 8 rows' loads issued before their sums (HBM latency)
+      const bool live = 4 * lane < A.q;
+      const float* base = img + 4 * lane;
+      int i = i0;
+      for (; i + 8 <= i1; i += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = live ? __ldg(reinterpret_cast<const float4*>(base + (int64_t)(i + u) * A.q)) : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc[0] += (double)v[u].x;
+          acc[1] += (double)v[u].y;
+          acc[2] += (double)v[u].z;
+          acc[3] += (double)v[u].w;
+        }
+      }
+      for (; i < i1; ++i) {
+        const float4 v = live ? __ldg(reinterpret_cast<const float4*>(base + (int64_t)i * A.q)) : make_float4(0, 0, 0, 0);
+        acc[0] += (double)v.x;
+        acc[1] += (double)v.y;
+        acc[2] += (double)v.z;
+        acc[3] += (double)v.w;
+      }
+    } else
     for (int i = i0; i < i1; ++i) {
       const float* row = img + (int64_t)i * A.q;
       if (vec) {
