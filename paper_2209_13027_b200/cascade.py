@@ -250,7 +250,7 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
         ld = _labels_dev(ex, lab[s0:s1])
         res = eng.fit(i1, i2, ld, ds.class_count, list(cfg.layers), bs, cfg.epsilon, n_global=n, first_sample=s0,
                       stage_hook=stage_hook)
-    bank = _bank_from_device(res.layers)
+        bank = _bank_from_device(res.layers)  # reads on the executor's stream
     object.__setattr__(bank, "_device_cache", (str(ex.device), res.layers))
     # the transform of the same samples reuses the uploaded images and the retained
     # last-hidden-layer maps (pipeline.compute_feature_counts)

@@ -80,7 +80,24 @@ def compute_feature_counts(ds, bank, config, executor=None, host_out=None):
             i1 = _to_dev32(ex, v1[s0:s1])
             i2 = _to_dev32(ex, v2[s0:s1])
         counts, plan = eng.transform_counts(i1, i2, layers, enc, bs, host_out=host_out)
+    handoff(ex, counts)
     return counts, plan
+
+
+def handoff(ex, *tensors) -> None:
+    """Stream-ordered handoff of device results to the caller's current stream.
+
+    The executor's stream is a non-blocking stream: without this, a caller that reads
+    a returned tensor on its own stream (e.g. ``.cpu()`` on the default stream) could
+    read it before the kernels writing it have finished.
+    """
+    import torch
+
+    cur = torch.cuda.current_stream(ex.device)
+    if cur != ex.stream:
+        cur.wait_stream(ex.stream)
+        for t in tensors:
+            t.record_stream(cur)
 
 
 def compute_features(ds, bank, config, executor=None) -> np.ndarray:
