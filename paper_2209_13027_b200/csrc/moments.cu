@@ -406,7 +406,13 @@ struct TmaBoxes {
   int rows_short, mb_short;  // short (single border row) tasks
   int shift;                 // columns the tile starts early so the box origin is 16 B aligned
   int ns;                    // ring depth (stages in flight)
+  int f64;                   // consumers convert each stage once into a float64 tile
 };
+
+// Named barrier over the consumer warps only (warps 0..G-1; the producer warp is not in it).
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
 
 // One launch per (view, task kind): the single tensor map is used directly from
 // the parameter space (no runtime selection of a tensor-map address).
@@ -475,18 +481,44 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
     const int cpart = lane + grp * KDX + bx.shift;
     const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
     const int kk = min(KDX, 2 * A.l2 - 1 - grp * KDX);  // live lags of this group
-    for (int s = 0; s < nstages; ++s) {
-      const int slot = s % NS;
-      mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
-      const float* tile = stage_mem + slot * max_stage;
-      const int64_t ms = ma + (int64_t)s * mb;
-      const int nm = (int)min((int64_t)mb, mbnd - ms);
-      for (int j = 0; j < nm; ++j) {
-        const float* t = tile + j * tile_elems;
-        lag_map<L1, TCB>(t, TCB, nrows, cown, cpart, short_task, skip0, kk, acc);
+    if (bx.f64) {
+      // convert each landed float32 stage once into a float64 tile shared by all consumer
+      // warps (every element is read by ~l2 + 2 threads: one conversion instead of one
+      // F2F per read on the FP64 pipe), release the float32 slot, then run the rings on doubles
+      double* t64 = reinterpret_cast<double*>(empty + NS);  // 16-byte aligned: 2 NS barriers after the stages
+      const int ctid = threadIdx.x, cthreads = G * 32;
+      for (int s = 0; s < nstages; ++s) {
+        const int slot = s % NS;
+        mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
+        const float* tile = stage_mem + slot * max_stage;
+        const int64_t ms = ma + (int64_t)s * mb;
+        const int nm = (int)min((int64_t)mb, mbnd - ms);
+        const int used = nm * tile_elems;
+        for (int e = 4 * ctid; e < used; e += 4 * cthreads) {  // tile_elems is a multiple of 4 (TCB % 4 == 0)
+          const float4 v = *reinterpret_cast<const float4*>(tile + e);
+          *reinterpret_cast<double2*>(t64 + e) = make_double2(v.x, v.y);
+          *reinterpret_cast<double2*>(t64 + e + 2) = make_double2(v.z, v.w);
+        }
+        consumer_sync(cthreads);
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        for (int j = 0; j < nm; ++j)
+          lag_map<L1, TCB>(t64 + j * tile_elems, TCB, nrows, cown, cpart, short_task, skip0, kk, acc);
+        consumer_sync(cthreads);  // t64 is rewritten by the next stage
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+    } else {
+      for (int s = 0; s < nstages; ++s) {
+        const int slot = s % NS;
+        mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
+        const float* tile = stage_mem + slot * max_stage;
+        const int64_t ms = ma + (int64_t)s * mb;
+        const int nm = (int)min((int64_t)mb, mbnd - ms);
+        for (int j = 0; j < nm; ++j) {
+          const float* t = tile + j * tile_elems;
+          lag_map<L1, TCB>(t, TCB, nrows, cown, cpart, short_task, skip0, kk, acc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
     }
     const int rslot = A.lane_slot[task * TILE_X + lane];
     const int xg = T.x0 + lane;
@@ -1131,7 +1163,9 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       }
       if (ok) {
         const size_t max_stage = (size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb;
-        const size_t tsmem = sizeof(float) * bx.ns * max_stage + 2 * bx.ns * sizeof(uint64_t);
+        bx.f64 = env_int("DDCCA_LAG_F32", 0) == 0 ? 1 : 0;
+        const size_t tsmem = sizeof(float) * bx.ns * max_stage + (2 * bx.ns + 1) * sizeof(uint64_t) +
+                             (bx.f64 ? sizeof(double) * max_stage : 0);
         dim3 tblock(32 * (P.G + 1));
         // task ids by kind, uploaded after the plan tables
         std::vector<int> ids_int, ids_short;
