@@ -454,6 +454,21 @@ static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cuda
     DDCCA_CH(9)
 #undef DDCCA_CH
   }
+  // 9..16 filters: 8-pixel strips in 128-thread CTAs (the 4-pixel / 256-thread table below
+  // spends one tap load per 8 FFMAs)
+  // (not for wide histograms: 2^n_bits shared bins per block would leave one small CTA per SM)
+  if (A.count > 8 && A.count <= 16 && !(HIST && A.nbits > 8) && !(ch8 && ch8[0] == '1')) {
+#define DDCCA_CH(L, NFV) \
+    if (l1 == L && l2 == L && A.count <= NFV && (HIST || NFV <= 12)) \
+      return run_shape<HIST, L, NFV, 8, 1, 128>(A, pack_host, st);
+    DDCCA_CH(7, 12)
+    DDCCA_CH(9, 12)
+    DDCCA_CH(3, 16)
+    DDCCA_CH(5, 16)
+    DDCCA_CH(7, 16)
+    DDCCA_CH(9, 16)
+#undef DDCCA_CH
+  }
 #define DDCCA_CC(L, NFV, PXV, PYV) \
   if (l1 == L && l2 == L && A.count <= NFV) return run_shape<HIST, L, NFV, PXV, PYV>(A, pack_host, st);
   DDCCA_CC(3, 8, 8, 1)
