@@ -456,6 +456,11 @@ static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cuda
   }
   // 9..16 filters: 8-pixel strips in 128-thread CTAs (the 4-pixel / 256-thread table below
   // spends one tap load per 8 FFMAs)
+  // wide histograms (2^n_bits > 256 shared bins per block): 8-pixel strips, 256-thread CTAs
+  if (HIST && A.nbits > 8 && A.count > 8 && A.count <= 12 && !(ch8 && ch8[0] == '1')) {
+    if (l1 == 7 && l2 == 7) return run_shape<true, 7, 12, 8, 1, 256>(A, pack_host, st);
+    if (l1 == 9 && l2 == 9) return run_shape<true, 9, 12, 8, 1, 256>(A, pack_host, st);
+  }
   // (not for wide histograms: 2^n_bits shared bins per block would leave one small CTA per SM)
   if (A.count > 8 && A.count <= 16 && !(HIST && A.nbits > 8) && !(ch8 && ch8[0] == '1')) {
 #define DDCCA_CH(L, NFV) \
