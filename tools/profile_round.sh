@@ -11,7 +11,7 @@ mkdir -p $OUT
 CMD="python bench.py --workload $WL --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > $OUT/plain.json 2> $OUT/plain.err || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"ddcca|lag_|conv|solve|zone_reduce|assemble|rect_sums|batch_epilogue|tree_level|hist|sym_eig|iq_" \
+    -k regex:"ddcca|lag_|conv|solve|whiten|finalize|zone_reduce|assemble|rect_sums|batch_epilogue|tree_level|hist|sym_eig|iq_" \
     --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"conv_hist_kernel" -s 2 -c 1 \
     -o $OUT/conv_hist $CMD > $OUT/ncu_full1.log 2>&1
