@@ -221,6 +221,13 @@ DDCCA_API int ddcca_nn_classify(const void* query, int64_t n_query, const void* 
 DDCCA_API int ddcca_counts_to_u16(const uint8_t* counts, int64_t n_blocks, int bins, int bpc, uint16_t* out,
                                   void* stream);
 
+/* ---------------------------------------------------------------------
+ * Second view (views.py:41-58): 8-neighbour LBP map of each (p, q) float32
+ * image, strict neighbour > centre, bits clockwise from the top-left,
+ * zero padding, code / 255; out may not alias images.
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_lbp(const float* images, int64_t n, int p, int q, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,7 @@ __all__ = [
     "conv_stack", "conv_plane", "layer_stats", "train", "forward_maps",
     "EncodeCfg", "block_origins", "sign_bits", "combine_bits", "block_iq",
     "encode_maps", "encode_pair", "feature_len", "features", "Pool",
-    "iq_lut", "block_counts", "nn_predict", "nn_accuracy",
+    "iq_lut", "block_counts", "nn_predict", "nn_accuracy", "lbp",
 ]
 
 
@@ -721,3 +721,24 @@ def nn_predict(train: np.ndarray, labels: np.ndarray, queries: np.ndarray, metri
 def nn_accuracy(pred: np.ndarray, labels: np.ndarray) -> float:
     """evaluate (classify.py:150-176): trace(confusion) / n."""
     return float(np.mean(np.asarray(pred) == np.asarray(labels)))
+
+
+# ---------------------------------------------------------------------------
+# second view (views.py:41-58)
+# ---------------------------------------------------------------------------
+
+_LBP_NEIGHBOURS = ((-1, -1), (-1, 0), (-1, 1), (0, 1), (1, 1), (1, 0), (1, -1), (0, -1))
+
+
+def lbp(img: np.ndarray) -> np.ndarray:
+    """8-neighbour LBP / 255: strict neighbour > centre, clockwise from the top-left, zero padding."""
+    x = np.asarray(img, dtype=np.float64)
+    if x.ndim != 2 or x.shape[0] < 3 or x.shape[1] < 3:
+        raise OracleShapeError(f"lbp needs at least a 3x3 image, got {x.shape}")
+    p, q = x.shape
+    pad = np.zeros((p + 2, q + 2))
+    pad[1:-1, 1:-1] = x
+    code = np.zeros((p, q))
+    for bit, (dy, dx) in enumerate(_LBP_NEIGHBOURS):
+        code += float(1 << bit) * (pad[1 + dy:1 + dy + p, 1 + dx:1 + dx + q] > x)
+    return code / 255.0

@@ -55,6 +55,7 @@ _SIGNATURES = {
     "ddcca_nn_workspace": (_sz, [_i64, _i64]),
     "ddcca_nn_classify": (_i32, [_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _i32, _vp, _vp, _sz, _vp]),
     "ddcca_counts_to_u16": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
+    "ddcca_lbp": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -113,13 +113,9 @@ def second_view_device(view1, kind: str, seed: int = 1, noise: float = 0.02):
     import torch
 
     if kind == "lbp":
-        n, p, q = view1.shape
-        pad = torch.zeros((n, p + 2, q + 2), dtype=torch.float32, device=view1.device)
-        pad[:, 1:-1, 1:-1] = view1
-        code = torch.zeros_like(view1)
-        for bit, (dy, dx) in enumerate(_LBP_OFFSETS):
-            code += float(1 << bit) * (pad[:, 1 + dy:1 + dy + p, 1 + dx:1 + dx + q] > view1).float()
-        return code / 255.0
+        from .views import lbp_stack
+
+        return lbp_stack(view1)  # the ddcca_lbp kernel (views.py:41-58)
     if kind in ("pair", "channel"):
         sm = view1.clone()
         sm[:, 1:-1, 1:-1] = (view1[:, :-2, 1:-1] + view1[:, 2:, 1:-1] + view1[:, 1:-1, :-2] + view1[:, 1:-1, 2:]

@@ -186,6 +186,7 @@ def main():
     v2 = f32(np.stack([dd.lbp_map(im) for im in v1]))
     run_pipeline("pipeline_orl_mini", v1, v2, labels, 4, [(4, 5, 5), (4, 5, 5)], 16, 7, 7)
     make_classify(dd)
+    make_views(dd)
     print("golden fixtures written to", OUT)
 
 
@@ -216,8 +217,26 @@ def make_classify(dd):
     np.savez_compressed(OUT / "classify.npz", **rec)
 
 
+def make_views(dd):
+    """Reference lbp_map (views.py:41-58) on float32-representable images with ties and negatives."""
+    from ddccanet import views as V
+
+    rng = np.random.default_rng(21)
+    rec = {}
+    shapes = [(3, 3), (5, 7), (16, 12), (9, 4)]
+    for k, (p, q) in enumerate(shapes):
+        img = rng.integers(-3, 6, size=(p, q)).astype(np.float32) / 4.0  # many exact ties, some negatives
+        if k == 2:
+            img = f32(rng.uniform(size=(p, q)))
+        rec[f"img{k}"] = img.astype(np.float64)
+        rec[f"lbp{k}"] = V.lbp_map(img.astype(np.float64))
+    np.savez_compressed(OUT / "views.npz", **rec)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["classify"]:
         make_classify(_import_reference())
+    elif sys.argv[1:] == ["views"]:
+        make_views(_import_reference())
     else:
         main()

@@ -225,3 +225,13 @@ def test_nn_classifier_golden(golden, metric):
     assert O.nn_accuracy(pred, orl["labels"][te]) == float(g[f"orl_acc_{metric}"])
     tie = O.nn_predict(g["tie_train"], g["tie_labels"], g["tie_queries"], metric)
     assert np.array_equal(tie, g[f"tie_pred_{metric}"])
+
+
+# ---------------------------------------------------------------- views
+
+def test_lbp_golden(golden):
+    g = golden("views")
+    for k in range(4):
+        assert np.array_equal(O.lbp(g[f"img{k}"]), g[f"lbp{k}"]), k
+    with pytest.raises(O.OracleShapeError):
+        O.lbp(np.zeros((2, 5)))
