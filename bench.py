@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--deterministic", type=int, default=1)
+    ap.add_argument("--moments", default="exact", choices=("exact", "blocked"),
+                    help="lag-product precision of layers >= 2 (ExecSettings.moments)")
     return ap.parse_args()
 
 
@@ -187,7 +189,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     nb = -(-M // bs)
     mine = shard_range(nb, rank, world)
     s0, s1 = mine.start * bs, min(M, mine.stop * bs)
-    ex = P.Executor(P.ExecSettings(deterministic=bool(args.deterministic)), device=local_rank)
+    ex = P.Executor(P.ExecSettings(deterministic=bool(args.deterministic), moments=args.moments), device=local_rank)
     layer_cfgs = [P.LayerConfig(L, P.PatchGeometry(l1, l2)) for L, l1, l2 in cfg["layers"]]
     enc = P.EncoderConfig(*cfg["block"])
 

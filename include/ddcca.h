@@ -92,6 +92,17 @@ DDCCA_API int ddcca_moments_partial(const float* maps1, const float* maps2, cons
                           int center, int class_count, double* partials, void* ws, size_t ws_bytes,
                           void* stream);
 
+/* Same, with flags. DDCCA_MOMENTS_F32_BLOCKS: the lag products of one map's
+ * row slab (<= 48 rows) accumulate in float32 and are added to the float64
+ * sums per map (FFMA instead of DFMA; ~1e-7 relative per lag sum instead of
+ * exact). Meant for layers whose inputs are filter responses (no DC term);
+ * applies to the TMA lag path (q % 4 == 0, 5x5 / 7x7 / 9x9), exact elsewhere. */
+#define DDCCA_MOMENTS_F32_BLOCKS 1
+DDCCA_API int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32_t* map_label,
+                             const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* g,
+                             int center, int class_count, double* partials, void* ws, size_t ws_bytes,
+                             int flags, void* stream);
+
 /* ---------------------------------------------------------------------
  * K9 — fixed left-to-right pairwise tree over n_parts payloads
  * Replaces: pairwise_merge (moments.py:132-144); merge (moments.py:113-129)

@@ -36,6 +36,8 @@ _SIGNATURES = {
     "ddcca_payload_len": (_i64, [_i32, _i32]),
     "ddcca_moments_workspace": (_sz, [_GP, _i32, _i64, _i32]),
     "ddcca_moments_partial": (_i32, [_vp, _vp, _vp, C.POINTER(_i64), _i32, _GP, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "ddcca_moments_partial_ex": (_i32, [_vp, _vp, _vp, C.POINTER(_i64), _i32, _GP, _i32, _i32, _vp, _vp, _sz,
+                                        _i32, _vp]),
     "ddcca_moments_tree": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "ddcca_accumulate_columns": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp]),
     "ddcca_solve_workspace": (_sz, [_i32]),

@@ -248,6 +248,66 @@ __device__ __forceinline__ void lag_map(const S* __restrict__ t, int tc, int nro
   }
 }
 
+// Blocked float32 form (layers whose inputs are filter responses): the products of one
+// map's rows accumulate in float32 (at most one slab, <= SLAB_ROWS terms per lag) and
+// the per-map partial is added to the float64 accumulator. Used only when the caller
+// asks for it (DDCCA_MOMENTS_F32_BLOCKS); float64 products are exact, these are not.
+template <int L1, int TC, bool SKIP0, int KK>
+__device__ __forceinline__ void lag_accumulate_f32(const float* __restrict__ t, int nrows, int cown, int cpart,
+                                                   double (&acc)[L1][KDX]) {
+  float fa[L1][KK];
+#pragma unroll
+  for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+    for (int k = 0; k < KK; ++k) fa[dy][k] = 0.f;
+  float ring[L1][KK];
+  const float* pp = t + cpart;
+#pragma unroll
+  for (int q = 0; q < L1 - 1; ++q)
+#pragma unroll
+    for (int k = 0; k < KK; ++k) ring[q][k] = pp[q * TC + k];
+  pp += (L1 - 1) * TC;
+  const float* po = t + cown;
+  for (int r0 = 0; r0 < nrows; r0 += L1) {
+#pragma unroll
+    for (int u = 0; u < L1; ++u) {
+      const int snew = (u + L1 - 1) % L1;
+#pragma unroll
+      for (int k = 0; k < KK; ++k) ring[snew][k] = pp[u * TC + k];
+      float own = po[u * TC];
+      own = (r0 + u < nrows) ? own : 0.f;
+#pragma unroll
+      for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy)
+#pragma unroll
+        for (int k = 0; k < KK; ++k) fa[dy][k] = fmaf(own, ring[(u + dy) % L1][k], fa[dy][k]);
+    }
+    pp += L1 * TC;
+    po += L1 * TC;
+  }
+#pragma unroll
+  for (int dy = 0; dy < L1; ++dy)
+#pragma unroll
+    for (int k = 0; k < KK; ++k) acc[dy][k] += (double)fa[dy][k];
+}
+
+template <int L1, int TC>
+__device__ __forceinline__ void lag_map_f32(const float* __restrict__ t, int nrows, int cown, int cpart,
+                                            bool short_task, bool skip0, int kk, double (&acc)[L1][KDX]) {
+  if (short_task) {  // single border rows: few products, keep them exact
+    if (kk >= 3) lag_accumulate_short<L1, TC, 3>(t, TC, nrows, cown, cpart, skip0, acc);
+    else if (kk == 2) lag_accumulate_short<L1, TC, 2>(t, TC, nrows, cown, cpart, skip0, acc);
+    else lag_accumulate_short<L1, TC, 1>(t, TC, nrows, cown, cpart, skip0, acc);
+  } else if (skip0) {
+    lag_accumulate_f32<L1, TC, true, 3>(t, nrows, cown, cpart, acc);
+  } else if (kk >= 3) {
+    lag_accumulate_f32<L1, TC, false, 3>(t, nrows, cown, cpart, acc);
+  } else if (kk == 2) {
+    lag_accumulate_f32<L1, TC, false, 2>(t, nrows, cown, cpart, acc);
+  } else {
+    lag_accumulate_f32<L1, TC, false, 1>(t, nrows, cown, cpart, acc);
+  }
+}
+
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   const int n = valid ? 4 : 0;  // src-size 0 => zero fill
@@ -407,6 +467,7 @@ struct TmaBoxes {
   int shift;                 // columns the tile starts early so the box origin is 16 B aligned
   int ns;                    // ring depth (stages in flight)
   int f64;                   // consumers convert each stage once into a float64 tile
+  int f32blocks;             // float32 products, per-map float32 partials (DDCCA_MOMENTS_F32_BLOCKS)
 };
 
 // Named barrier over the consumer warps only (warps 0..G-1; the producer warp is not in it).
@@ -481,7 +542,19 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
     const int cpart = lane + grp * KDX + bx.shift;
     const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
     const int kk = min(KDX, 2 * A.l2 - 1 - grp * KDX);  // live lags of this group
-    if (bx.f64) {
+    if (bx.f32blocks) {
+      for (int s = 0; s < nstages; ++s) {
+        const int slot = s % NS;
+        mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
+        const float* tile = stage_mem + slot * max_stage;
+        const int64_t ms = ma + (int64_t)s * mb;
+        const int nm = (int)min((int64_t)mb, mbnd - ms);
+        for (int j = 0; j < nm; ++j)
+          lag_map_f32<L1, TCB>(tile + j * tile_elems, nrows, cown, cpart, short_task, skip0, kk, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+    } else if (bx.f64) {
       // convert each landed float32 stage once into a float64 tile shared by all consumer
       // warps (every element is read by ~l2 + 2 threads: one conversion instead of one
       // F2F per read on the FP64 pipe), release the float32 slot, then run the rings on doubles
@@ -1056,6 +1129,15 @@ size_t ddcca_moments_workspace(const ddcca_geom* gg, int n_batches, int64_t max_
 int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t* map_label,
                           const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* gg, int center,
                           int class_count, double* partials, void* ws, size_t ws_bytes, void* stream) {
+  return ddcca_moments_partial_ex(maps1, maps2, map_label, batch_offsets_host, n_batches, gg, center, class_count,
+                                  partials, ws, ws_bytes, 0, stream);
+}
+
+int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32_t* map_label,
+                             const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* gg, int center,
+                             int class_count, double* partials, void* ws, size_t ws_bytes, int flags,
+                             void* stream) {
+  if (flags & ~DDCCA_MOMENTS_F32_BLOCKS) return fail(DDCCA_ECONFIG, "unknown moments flags 0x%x", flags);
   Geo g;
   DDCCA_TRY(make_geo(gg, &g));
   if (n_batches < 1) return fail(DDCCA_ECONFIG, "no batches to accumulate");
@@ -1164,6 +1246,7 @@ int ddcca_moments_partial(const float* maps1, const float* maps2, const int32_t*
       if (ok) {
         const size_t max_stage = (size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb;
         bx.f64 = env_int("DDCCA_LAG_F32", 0) == 0 ? 1 : 0;
+        bx.f32blocks = (flags & DDCCA_MOMENTS_F32_BLOCKS) ? 1 : 0;
         const size_t tsmem = sizeof(float) * bx.ns * max_stage + (2 * bx.ns + 1) * sizeof(uint64_t) +
                              (bx.f64 ? sizeof(double) * max_stage : 0);
         dim3 tblock(32 * (P.G + 1));

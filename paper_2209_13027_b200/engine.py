@@ -33,6 +33,7 @@ from .patches import PatchGeometry
 
 MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
 KEEP_MAPS_BYTES = 48 << 30  # fit keeps the last layer's input maps (both views) for the transform if they fit
+MOMENTS_F32_BLOCKS = 1  # ddcca.h DDCCA_MOMENTS_F32_BLOCKS
 HOST_CHUNK_BATCHES = 4  # sample batches per streamed device->host count copy
 
 
@@ -75,7 +76,7 @@ def payload_len(dim: int, classes: int) -> int:
 
 
 def moments_partials(ex, maps1, maps2, map_labels, batch_offsets: np.ndarray, geom: PatchGeometry, center: bool,
-                     classes: int, out=None):
+                     classes: int, out=None, flags: int = 0):
     """Per-batch partial accumulators (n_batches, payload_len) float64 on device."""
     torch = _torch()
     lib = _native.load()
@@ -91,10 +92,10 @@ def moments_partials(ex, maps1, maps2, map_labels, batch_offsets: np.ndarray, ge
     if out is None:
         out = torch.empty((nb, plen), dtype=torch.float64, device=ex.device)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=ex.device)
-    rc = lib.ddcca_moments_partial(_native.ptr(maps1), _native.ptr(maps2), _native.ptr(map_labels),
-                                   offs.ctypes.data_as(C.POINTER(C.c_int64)), nb, C.byref(g), int(bool(center)),
-                                   classes, _native.ptr(out), _native.ptr(ws), ws_bytes,
-                                   _native.stream_ptr(ex.stream))
+    rc = lib.ddcca_moments_partial_ex(_native.ptr(maps1), _native.ptr(maps2), _native.ptr(map_labels),
+                                      offs.ctypes.data_as(C.POINTER(C.c_int64)), nb, C.byref(g), int(bool(center)),
+                                      classes, _native.ptr(out), _native.ptr(ws), ws_bytes, int(flags),
+                                      _native.stream_ptr(ex.stream))
     _native.check(rc, "moments")
     return out
 
@@ -453,12 +454,17 @@ class Engine:
             self._timed(f"moments_l{len(layers) + 1}", 5, {"kind": "fp64", "flops": fl, "gram_flops": gfl,
                                                           "bytes": 8.0 * nmaps * p * q},
                         moments_partials, ex, m1, m2, mlab, offs, geom, center, classes,
-                        out=parts[row:row + len(group)])
+                        out=parts[row:row + len(group)], flags=self.moments_flags(layers))
             row += len(group)
         if keep_buf is not None:
             self.maps_cache = {"key": self._cache_key(images1, layers), "m1": keep_buf[0], "m2": keep_buf[1],
                                "n_in": n_in}
         return parts
+
+    def moments_flags(self, layers: list) -> int:
+        """Float32-blocked lag products for layers fed by filter responses (ExecSettings.moments)."""
+        mode = getattr(self.ex.settings, "moments", "exact")
+        return MOMENTS_F32_BLOCKS if (layers and mode == "blocked") else 0
 
     def reduce_partials(self, parts, n_global_batches: int, local_batches: range):
         """Merged accumulator over all ranks' batches (fixed tree or sum-allreduce)."""

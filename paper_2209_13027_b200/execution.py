@@ -19,6 +19,9 @@ from dataclasses import dataclass
 from .errors import ConfigError
 
 
+MOMENT_MODES = ("exact", "blocked")
+
+
 @dataclass(frozen=True)
 class ExecSettings:
     """Same fields as the reference (execution.py:15-23).
@@ -28,15 +31,22 @@ class ExecSettings:
     selects the reduction: True -> per-batch partials gathered from all ranks
     and merged through the reference's fixed left-to-right tree (bitwise
     independent of the GPU count); False -> local tree + one sum-allreduce.
+    ``moments`` (B200 addition): "exact" -> every lag product in float64 (exact
+    for float32 maps); "blocked" -> layers fed by filter responses accumulate
+    each map's products in float32 and add the per-map partials in float64
+    (~1e-7 relative per statistic, 2x the arithmetic rate; layer 1 stays exact).
     """
 
     threads: int = 1
     deterministic: bool = True
     seed: int = 0
+    moments: str = "exact"
 
     def __post_init__(self):
         if self.threads < 1:
             raise ConfigError(f"thread count {self.threads} must be >= 1")
+        if self.moments not in MOMENT_MODES:
+            raise ConfigError(f"moments mode {self.moments!r} not one of {MOMENT_MODES}")
 
 
 class Executor:

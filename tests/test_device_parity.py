@@ -466,3 +466,23 @@ def test_two_ranks_match_one_rank():
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "det=True: ranks 2, checked OK" in r.stdout and "det=False: ranks 2, checked OK" in r.stdout
+
+
+@pytest.mark.parametrize("l,p,q", [(7, 40, 36), (5, 28, 24), (9, 36, 40)])
+def test_blocked_moments_close_to_exact(ex, l, p, q):
+    """ExecSettings(moments="blocked"): float32 per-map lag products, statistics within 1e-7 of the exact ones."""
+    rng = np.random.default_rng(l + p)
+    n_maps, nb = 24, 3
+    m1 = torch.from_numpy(rng.standard_normal((n_maps, p, q)).astype(np.float32)).to(ex.device)
+    m2 = torch.from_numpy(rng.standard_normal((n_maps, p, q)).astype(np.float32)).to(ex.device)
+    lab = torch.from_numpy((np.arange(n_maps) % 3).astype(np.int32)).to(ex.device)
+    offs = np.arange(0, n_maps + 1, n_maps // nb, dtype=np.int64)
+    geom = P.PatchGeometry(l, l)
+    with torch.cuda.stream(ex.stream):
+        a = E.moments_partials(ex, m1, m2, lab, offs, geom, True, 3).cpu().numpy()
+        b = E.moments_partials(ex, m1, m2, lab, offs, geom, True, 3, flags=E.MOMENTS_F32_BLOCKS).cpu().numpy()
+    d = l * l
+    for lo, hi in ((0, d * d), (d * d, 2 * d * d)):
+        err = np.linalg.norm(a[:, lo:hi] - b[:, lo:hi]) / np.linalg.norm(a[:, lo:hi])
+        assert 0 < err <= 1e-7, err  # nonzero: the float32 path really ran
+    assert np.array_equal(a[:, 2 * d * d:], b[:, 2 * d * d:])  # sums / counts stay exact
