@@ -118,10 +118,11 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
 
 template <int NF, int PX, int PY>
 __device__ __forceinline__ unsigned cc_code(const float (&acc)[PY][PX][NF], int y, int j, int count) {
+  // filters g >= count have all-zero taps, so their response is +0 and their bit is 0
   unsigned code = 0;
 #pragma unroll
   for (int g = 0; g < NF; ++g)
-    if (g < count && acc[y][j][g] > 0.f) code |= 1u << g;
+    if (acc[y][j][g] > 0.f) code |= 1u << g;
   return code;
 }
 
@@ -279,6 +280,20 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
       float acc[PY][PX][NF];
       cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
       const int bx0 = v0 / A.bw, rem0 = v0 - bx0 * A.bw;
+      if (v0 + PX <= cols && rem0 + PX <= A.bw) {
+        // whole strip inside one block: no per-pixel bounds or block stepping
+#pragma unroll
+        for (int y = 0; y < PY; ++y)
+          if (r + y < band_rows) {
+            unsigned* bb = bins + ((r + y) / A.bh * A.nbx + bx0) * words;
+#pragma unroll
+            for (int j = 0; j < PX; ++j) {
+              const unsigned code = cc_code<NF, PX, PY>(acc, y, j, A.count);
+              atomicAdd(&bb[code >> 1], 1u << ((code & 1u) << 4));
+            }
+          }
+        continue;
+      }
 #pragma unroll
       for (int y = 0; y < PY; ++y)
         if (r + y < band_rows) {
