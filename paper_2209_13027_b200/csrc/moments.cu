@@ -494,7 +494,8 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
   const int mb = short_task ? bx.mb_short : bx.mb_int;
   const int tile_elems = trb * TCB;
   const int stage_elems = mb * tile_elems;
-  const int max_stage = max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * TCB;
+  // stage slots 128-byte aligned: the TMA destination of every slot must be
+  const int max_stage = (max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * TCB + 31) / 32 * 32;
   const int NS = bx.ns;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_mem + NS * max_stage);
   uint64_t* empty = full + NS;
@@ -1244,7 +1245,8 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
              make_map(&tm[2 + v], base, n_maps, g.p, g.q, tcb, bx.rows_short, bx.mb_short);
       }
       if (ok) {
-        const size_t max_stage = (size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb;
+        const size_t max_stage =
+            ((size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb + 31) / 32 * 32;
         bx.f64 = env_int("DDCCA_LAG_F32", 0) == 0 ? 1 : 0;
         bx.f32blocks = (flags & DDCCA_MOMENTS_F32_BLOCKS) ? 1 : 0;
         const size_t tsmem = sizeof(float) * bx.ns * max_stage + (2 * bx.ns + 1) * sizeof(uint64_t) +
