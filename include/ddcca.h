@@ -239,6 +239,17 @@ DDCCA_API int ddcca_counts_to_u16(const uint8_t* counts, int64_t n_blocks, int b
  * ------------------------------------------------------------------- */
 DDCCA_API int ddcca_lbp(const float* images, int64_t n, int p, int q, float* out, void* stream);
 
+/* ---------------------------------------------------------------------
+ * Host ingestion (dataset.py:68-118): binary PGM (P5) decode, values /
+ * maxval (8-bit, or big-endian 16-bit when maxval > 255), '#' comments in
+ * the header. ddcca_pgm_load_many decodes n same-size files in parallel
+ * (threads) into out[n][height][width] float32 (pinned host memory works).
+ * Host-only: no GPU needed. Errors: DDCCA_ESHAPE + ddcca_last_error().
+ * ------------------------------------------------------------------- */
+DDCCA_API int ddcca_pgm_info(const char* path, int* width, int* height, int* maxval, int64_t* payload_offset);
+DDCCA_API int ddcca_pgm_load_many(const char* const* paths, int64_t n, int height, int width, float* out,
+                                  int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -187,6 +187,7 @@ def main():
     run_pipeline("pipeline_orl_mini", v1, v2, labels, 4, [(4, 5, 5), (4, 5, 5)], 16, 7, 7)
     make_classify(dd)
     make_views(dd)
+    make_io(dd)
     print("golden fixtures written to", OUT)
 
 
@@ -233,8 +234,43 @@ def make_views(dd):
     np.savez_compressed(OUT / "views.npz", **rec)
 
 
+def make_io(dd):
+    """PGM files + manifests written by the reference, and its load_pgm / load_dataset outputs."""
+    from ddccanet import dataset as D
+    from ddccanet import views as V
+
+    io = OUT / "io"
+    io.mkdir(exist_ok=True)
+    rng = np.random.default_rng(33)
+    rec = {}
+    names = []
+    for k in range(6):
+        img = rng.uniform(size=(6, 5))
+        name = f"img{k}.pgm"
+        D.write_pgm(io / name, img, maxval=255 if k % 3 else 4000)  # 8-bit and big-endian 16-bit
+        names.append(name)
+    # a header with comments and odd whitespace
+    (io / "comment.pgm").write_bytes(b"P5\n# made by hand\n5 6 # width height\n\t255\n" + bytes(range(30)))
+    (io / "bad_magic.pgm").write_bytes(b"P2\n2 2\n255\n1 2 3 4")
+    (io / "truncated.pgm").write_bytes(b"P5\n4 4\n255\n" + bytes(10))
+    for name in names + ["comment.pgm"]:
+        rec["pgm_" + name] = D.load_pgm(io / name)
+    (io / "pairs.txt").write_text("# two views per line\n" + "\n".join(
+        f"{names[2 * i]},{names[2 * i + 1]},{[7, 3, 7][i]}" for i in range(3)) + "\n")
+    (io / "gray.txt").write_text("\n".join(f"{n},{[5, 9, 5, 2, 9, 2][i]}" for i, n in enumerate(names)) + "\n")
+    ds = D.load_dataset(io / "pairs.txt")
+    rec["pairs_v1"], rec["pairs_v2"], rec["pairs_labels"] = ds.view_stack(1), ds.view_stack(2), ds.labels
+    rec["pairs_map"] = np.array(sorted(ds.label_map.items()))
+    ds = D.load_dataset(io / "gray.txt", V.ViewRecipe("lbp_plus_gray"))
+    rec["gray_v1"], rec["gray_v2"], rec["gray_labels"] = ds.view_stack(1), ds.view_stack(2), ds.labels
+    rec["gray_map"] = np.array(sorted(ds.label_map.items()))
+    np.savez_compressed(OUT / "io.npz", **rec)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["classify"]:
+    if sys.argv[1:] == ["io"]:
+        make_io(_import_reference())
+    elif sys.argv[1:] == ["classify"]:
         make_classify(_import_reference())
     elif sys.argv[1:] == ["views"]:
         make_views(_import_reference())
