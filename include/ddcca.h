@@ -250,6 +250,14 @@ DDCCA_API int ddcca_pgm_info(const char* path, int* width, int* height, int* max
 DDCCA_API int ddcca_pgm_load_many(const char* const* paths, int64_t n, int height, int width, float* out,
                                   int threads);
 
+/* Feature CSV (run_extract, pipeline.py:143-166) straight from host block
+ * counts: row r is "first_index + r,v,v,...\n" with v = lut_str[count]
+ * (the caller's format(lut[k], ".17g") strings for k = 0..bpc). Count kinds as
+ * ddcca_block_hist; `bins` per block. Host-only, `threads` formatting workers. */
+DDCCA_API int ddcca_write_feature_csv(const void* counts, int count_kind, int64_t rows, int64_t cols, int bins,
+                                      int bpc, const char* const* lut_str, const int* lut_len,
+                                      int64_t first_index, const char* path, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,8 @@ _SIGNATURES = {
     "ddcca_lbp": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "ddcca_pgm_info": (_i32, [C.c_char_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i64)]),
     "ddcca_pgm_load_many": (_i32, [C.POINTER(C.c_char_p), _i64, _i32, _i32, _vp, _i32]),
+    "ddcca_write_feature_csv": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, C.POINTER(C.c_char_p), C.POINTER(_i32),
+                                       _i64, C.c_char_p, _i32]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

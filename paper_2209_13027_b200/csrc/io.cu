@@ -174,3 +174,71 @@ int ddcca_pgm_load_many(const char* const* paths, int64_t n, int height, int wid
 }
 
 }  // extern "C"
+
+// ----------------------------------------------------------------------------
+// Feature CSV writer (run_extract, pipeline.py:143-166): one line per sample,
+// "index,v0,v1,..." with every value formatted by the caller as Python's
+// format(v, ".17g"). The values are IQ features of block counts, so the caller
+// passes the formatted string of each LUT entry (count 0 .. bpc) once and the
+// writer only copies strings: rows are formatted by `threads` workers in blocks
+// and written in order. Counts: kind 0 u8, 1 saturating u8 (255 = the block
+// remainder), 2 u16; bins per block = `bins`, `bpc` pixels per block.
+// ----------------------------------------------------------------------------
+namespace ddcca {
+
+static inline unsigned count_at(const void* counts, int kind, int64_t row, int64_t col, int64_t cols, int bins,
+                                int bpc) {
+  if (kind == 2) return static_cast<const uint16_t*>(counts)[row * cols + col];
+  const uint8_t* r = static_cast<const uint8_t*>(counts) + row * cols;
+  unsigned c = r[col];
+  if (kind == 1 && c == 255) {
+    const int64_t b0 = col / bins * bins;
+    unsigned s = 0;
+    for (int k = 0; k < bins; ++k) s += r[b0 + k];
+    c = 255 + (unsigned)(bpc - (int)s);
+  }
+  return c;
+}
+
+}  // namespace ddcca
+
+extern "C" int ddcca_write_feature_csv(const void* counts, int count_kind, int64_t rows, int64_t cols, int bins,
+                                       int bpc, const char* const* lut_str, const int* lut_len, int64_t first_index,
+                                       const char* path, int threads) {
+  if (rows < 0 || cols < 1 || bins < 1 || bpc < 1 || count_kind < 0 || count_kind > 2)
+    return fail(DDCCA_ESHAPE, "feature csv: bad shape");
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(DDCCA_ESHAPE, "cannot write %s", path);
+  const int nt = std::max(1, std::min(threads, 64));
+  const int64_t block = 16;  // rows per work item
+  const int64_t nblocks = (rows + block - 1) / block;
+  std::vector<std::string> out(nt);
+  bool ok = true;
+  for (int64_t b0 = 0; b0 < nblocks && ok; b0 += nt) {
+    std::vector<std::thread> pool;
+    auto fmt = [&](int t) {
+      const int64_t b = b0 + t;
+      std::string& s = out[t];
+      s.clear();
+      if (b >= nblocks) return;
+      for (int64_t r = b * block; r < std::min(rows, (b + 1) * block); ++r) {
+        s += std::to_string(first_index + r);
+        for (int64_t c = 0; c < cols; ++c) {
+          const unsigned k = count_at(counts, count_kind, r, c, cols, bins, bpc);
+          s += ',';
+          if (k <= (unsigned)bpc) s.append(lut_str[k], (size_t)lut_len[k]);
+          else s += "nan";
+        }
+        s += '\n';
+      }
+    };
+    for (int t = 1; t < nt; ++t) pool.emplace_back(fmt, t);
+    fmt(0);
+    for (auto& th : pool) th.join();
+    for (int t = 0; t < nt && ok; ++t)
+      if (!out[t].empty() && std::fwrite(out[t].data(), 1, out[t].size(), f) != out[t].size()) ok = false;
+  }
+  if (std::fclose(f) != 0) ok = false;
+  if (!ok) return fail(DDCCA_ESHAPE, "cannot write %s", path);
+  return DDCCA_OK;
+}

@@ -111,3 +111,32 @@ def compute_features(ds, bank, config, executor=None) -> np.ndarray:
         feats = E.Engine(ex).expand(counts, plan, enc)
         out = feats.cpu().numpy()
     return out
+
+
+def write_feature_csv(path, counts, plan, enc, first_index: int = 0, threads: int = 16) -> None:
+    """Feature CSV of run_extract (pipeline.py:143-166) from block counts, without float64 features.
+
+    One line per sample: ``index,v0,v1,...`` with every value as Python's
+    ``format(v, ".17g")`` of the IQ feature; the 17-digit strings of the
+    bpc + 1 LUT values are formatted here once and the native writer
+    (``ddcca_write_feature_csv``) copies them per count with ``threads``
+    workers. ``counts``: (m, featlen) host array / tensor (u8, saturating u8
+    or u16 as ``compute_feature_counts`` returns them).
+    """
+    import ctypes as C
+
+    from . import _native
+
+    c = counts.cpu().numpy() if hasattr(counts, "cpu") else np.asarray(counts)
+    c = np.ascontiguousarray(c)
+    kind = E.count_kind(plan.bpc)
+    if kind == 2:
+        c = c.view(np.uint16)
+    lut = E.iq_lut(enc)
+    strs = [format(float(v), ".17g").encode("ascii") for v in lut]
+    arr = (C.c_char_p * len(strs))(*strs)
+    lens = (C.c_int * len(strs))(*[len(x) for x in strs])
+    rows, cols = c.shape
+    _native.check(_native.load().ddcca_write_feature_csv(c.ctypes.data_as(C.c_void_p), kind, rows, cols, plan.bins,
+                                                         plan.bpc, arr, lens, int(first_index), str(path).encode(),
+                                                         int(threads)), "write_feature_csv")

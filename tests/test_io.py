@@ -85,3 +85,23 @@ def test_load_dataset_errors(tmp_path):
     (tmp_path / "missing.txt").write_text(f"{tmp_path / 'nope.pgm'},1\n")
     with pytest.raises((P.IoError, P.ParseError)):
         P.load_dataset(tmp_path / "missing.txt")
+
+
+@pytest.mark.parametrize("bh,bw", [(4, 4), (16, 17), (10, 30)])  # u8, saturating u8, u16 counts
+def test_feature_csv_matches_reference_format(tmp_path, bh, bw):
+    """Native CSV writer == the reference's f"{i}," + ",".join(format(v, ".17g")) lines on the float64 features."""
+    import paper_2209_13027_b200 as P
+    from paper_2209_13027_b200 import engine as E
+
+    rng = np.random.default_rng(bh + bw)
+    enc = P.EncoderConfig(bh, bw)
+    plan = E.block_plan(enc, 40, 60, 4)
+    n = 7
+    counts = np.stack([np.concatenate([np.bincount(rng.integers(0, 16, plan.bpc), minlength=16)
+                                       for _ in range(plan.blocks)]) for _ in range(n)])
+    kind = E.count_kind(plan.bpc)
+    stored = counts.astype(np.uint16).view(np.int16) if kind == 2 else np.minimum(counts, 255).astype(np.uint8)
+    P.write_feature_csv(tmp_path / "f.csv", stored, plan, enc, first_index=3, threads=3)
+    feats = E.iq_lut(enc)[counts]
+    want = "".join(f"{i + 3}," + ",".join(format(v, ".17g") for v in row) + "\n" for i, row in enumerate(feats))
+    assert (tmp_path / "f.csv").read_text() == want
