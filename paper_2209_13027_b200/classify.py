@@ -48,11 +48,12 @@ class ClassifierModel:
     class_count: int
     metric: str = "euclidean"
     lam: float = 0.0
-    train_features: object | None = None  # device rows (float64 / u8 / u16)
+    train_features: object | None = None  # device rows (float64 / u8 / u16), host float64 rows, or CountFeatures
     train_labels: np.ndarray | None = None
     weights: np.ndarray | None = None
     row_kind: int = 3
     lut: object | None = None  # device LUT for count rows
+    count_source: object | None = None  # the CountFeatures the rows came from (model files write their values)
 
     @property
     def feature_dim(self) -> int:
@@ -137,7 +138,8 @@ def fit(features, labels, kind: str = "nearest_neighbor", metric: str = "euclide
     ex = _executor(executor)
     rows, row_kind, lut = _rows(ex, features)
     return ClassifierModel(kind=kind, class_count=class_count, metric=metric, train_features=rows,
-                           train_labels=labels.copy(), row_kind=row_kind, lut=lut)
+                           train_labels=labels.copy(), row_kind=row_kind, lut=lut,
+                           count_source=features if isinstance(features, CountFeatures) else None)
 
 
 def predict_many(model: ClassifierModel, features, executor=None) -> np.ndarray:
@@ -145,6 +147,11 @@ def predict_many(model: ClassifierModel, features, executor=None) -> np.ndarray:
     import torch
 
     ex = _executor(executor)
+    if model.kind != "nearest_neighbor":
+        raise ConfigError("ridge_one_vs_all prediction is not on the device path (nearest_neighbor only)")
+    if not hasattr(model.train_features, "data_ptr"):  # e.g. a loaded model: float64 rows on the host
+        rows, model.row_kind, model.lut = _rows(ex, model.train_features)
+        model.train_features = rows
     q, q_kind, _ = _rows(ex, features)
     if q.ndim != 2 or q.shape[1] != model.feature_dim:
         raise ShapeError(f"feature dim {q.shape[-1] if q.ndim else '?'} does not match model dim {model.feature_dim}")

@@ -188,6 +188,7 @@ def main():
     make_classify(dd)
     make_views(dd)
     make_io(dd)
+    make_models(dd)
     print("golden fixtures written to", OUT)
 
 
@@ -267,8 +268,30 @@ def make_io(dd):
     np.savez_compressed(OUT / "io.npz", **rec)
 
 
+def make_models(dd):
+    """Model files written by the reference's save_model (NN and ridge classifiers)."""
+    from ddccanet import classify as Cl
+    from ddccanet import model_io as M
+
+    small = np.load(OUT / "pipeline_small.npz")
+    layers = []
+    for i, (L, l1, l2) in enumerate(small["layers"]):
+        layers.append(dd.FilterLayer(filters1=small[f"f1_{i}"], filters2=small[f"f2_{i}"],
+                                     geom=dd.PatchGeometry(int(l1), int(l2)), center=True))
+    bank = dd.FilterBank(layers=tuple(layers))
+    feats, labels = small["features"], small["labels"].astype(np.int64)
+    snap = {"net.batch": "8", "encoder.block": "4 4", "data.recipe": "external_pair"}
+    nn = Cl.fit(feats, labels, kind="nearest_neighbor", metric="cosine")
+    M.save_model(M.ModelArtifact(snapshot=snap, bank=bank, classifier=nn, label_map={5: 0, 2: 1, 9: 2}),
+                 OUT / "model_nn.txt")
+    ridge = Cl.fit(feats[:, :20], labels, kind="ridge_one_vs_all")
+    M.save_model(M.ModelArtifact(snapshot=snap, bank=bank, classifier=ridge), OUT / "model_ridge.txt")
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["io"]:
+    if sys.argv[1:] == ["models"]:
+        make_models(_import_reference())
+    elif sys.argv[1:] == ["io"]:
         make_io(_import_reference())
     elif sys.argv[1:] == ["classify"]:
         make_classify(_import_reference())
