@@ -19,9 +19,9 @@
 
 namespace ddcca {
 
-constexpr int NN_T = 64;        // query / train rows per tile
-constexpr int NN_K = 32;        // features per stage
-constexpr int NN_THREADS = 256; // 16 x 16 threads, 4 x 4 outputs each
+constexpr int NN_T = 128;       // query / train rows per tile
+constexpr int NN_K = 16;        // features per stage
+constexpr int NN_THREADS = 256; // 16 x 16 threads, 8 x 8 outputs each
 
 template <int KIND>
 __device__ __forceinline__ double nn_elem(const void* rows, int64_t idx, const double* lut) {
@@ -50,17 +50,6 @@ __global__ void nn_norms_kernel(const void* rows, int64_t n, int64_t dim, const 
   }
 }
 
-template <int KIND>
-__device__ __forceinline__ void nn_stage(const void* rows, int64_t n, int64_t dim, int64_t r0, int64_t k0,
-                                         const double* lut, double (*dst)[NN_T + 2]) {
-  // NN_T rows x NN_K features -> dst[k][row] (float64), zeros outside
-  for (int e = threadIdx.x; e < NN_T * NN_K; e += NN_THREADS) {
-    const int r = e / NN_K, k = e % NN_K;  // consecutive threads walk one row's features (coalesced)
-    const int64_t gr = r0 + r, gk = k0 + k;
-    dst[k][r] = (gr < n && gk < dim) ? nn_elem<KIND>(rows, gr * dim + gk, lut) : 0.0;
-  }
-}
-
 struct NnCand {
   double dist;
   int64_t label;
@@ -70,58 +59,137 @@ __device__ __forceinline__ bool nn_better(double d, int64_t l, double bd, int64_
   return d < bd || (d == bd && l < bl);
 }
 
+// One row's NN_K features [k0, k0 + NN_K) held in registers between stages:
+// integer counts for KIND 0 / 2, float64 values for KIND 3; zeros outside the matrix.
 template <int KIND>
-__global__ void __launch_bounds__(NN_THREADS)
+struct NnRaw {
+  unsigned c[KIND == 3 ? 1 : NN_K];
+  double d[KIND == 3 ? NN_K : 1];
+};
+
+template <int KIND>
+__device__ __forceinline__ void nn_fetch(const void* rows, int64_t n, int64_t dim, int64_t row, int64_t k0,
+                                         NnRaw<KIND>& raw) {
+  constexpr int ES = KIND == 0 ? 1 : (KIND == 2 ? 2 : 8);
+  const bool full = row < n && k0 + NN_K <= dim && ((dim * ES) & 15) == 0;
+  const char* base = static_cast<const char*>(rows) + (row * dim + k0) * ES;
+  if (full) {
+    const uint4* src = reinterpret_cast<const uint4*>(base);
+    if (KIND == 0) {
+      const uint4 v = __ldg(src);
+      const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < NN_K; ++k) raw.c[k] = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
+    } else if (KIND == 2) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 v = __ldg(src + h);
+        const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) raw.c[8 * h + k] = (w[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NN_K; ++k) raw.d[k] = __ldg(reinterpret_cast<const double*>(base) + k);
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < NN_K; ++k) {
+    const bool in = row < n && k0 + k < dim;
+    if (KIND == 0) raw.c[k] = in ? static_cast<const uint8_t*>(rows)[row * dim + k0 + k] : 0u;
+    else if (KIND == 2) raw.c[k] = in ? static_cast<const uint16_t*>(rows)[row * dim + k0 + k] : 0u;
+    else raw.d[k] = in ? static_cast<const double*>(rows)[row * dim + k0 + k] : 0.0;
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void nn_store(const NnRaw<KIND>& raw, const double* lut, double (*dst)[NN_T + 2], int r,
+                                         bool live, int64_t kvalid) {
+  // out-of-range rows / features hold count 0 -> lut[0]; force exact zeros for them
+#pragma unroll
+  for (int k = 0; k < NN_K; ++k) {
+    double v;
+    if (KIND == 0) v = lut[raw.c[k]];
+    else if (KIND == 2) v = __ldg(lut + raw.c[k]);
+    else v = raw.d[k];
+    dst[k][r] = (live && k < kvalid) ? v : 0.0;
+  }
+}
+
+// One CTA = NN_T queries x NN_T training rows over the whole feature dimension,
+// 8 x 8 outputs per thread (rows ty*2 + {0,1} + 32 i, columns tx*2 + {0,1} + 32 j),
+// double-buffered shared tiles filled from registers fetched one stage ahead.
+template <int KIND>
+__global__ void __launch_bounds__(NN_THREADS, 1)
     nn_tile_kernel(const void* query, int64_t nq, const void* train, int64_t nt, int64_t dim,
                    const double* __restrict__ lut_g, int lut_len, const double* __restrict__ qn,
                    const double* __restrict__ tn, const int64_t* __restrict__ labels, int metric,
                    NnCand* __restrict__ cand) {
-  __shared__ __align__(16) double As[NN_K][NN_T + 2];
-  __shared__ __align__(16) double Bs[NN_K][NN_T + 2];
-  __shared__ double lut[KIND == 0 ? 256 : 1];  // u8 LUT in shared memory; u16 reads the (L1-cached) global one
-  static_assert(NN_K * (NN_T + 2) >= NN_T * 16, "candidate scratch aliases the staging tiles");
-  double (*red_d)[16] = reinterpret_cast<double (*)[16]>(&As[0][0]);
-  int64_t (*red_l)[16] = reinterpret_cast<int64_t (*)[16]>(&Bs[0][0]);
+  extern __shared__ __align__(16) double nn_sm[];
+  double (*As)[NN_T + 2] = reinterpret_cast<double (*)[NN_T + 2]>(nn_sm);                  // [2][NN_K][NN_T+2]
+  double (*Bs)[NN_T + 2] = reinterpret_cast<double (*)[NN_T + 2]>(nn_sm + 2 * NN_K * (NN_T + 2));
+  double* lut = nn_sm + 4 * NN_K * (NN_T + 2);
   const double* L = lut_g;
   if (KIND == 0) {
     for (int i = threadIdx.x; i < lut_len; i += NN_THREADS) lut[i] = lut_g[i];
     L = lut;
   }
   const int64_t q0 = (int64_t)blockIdx.y * NN_T, t0 = (int64_t)blockIdx.x * NN_T;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // outputs: rows ty*4.., cols tx*4..
-  double acc[4][4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // staging roles: threads 0..127 fetch query rows, 128..255 training rows
+  const bool stage_q = threadIdx.x < NN_T;
+  const int srow = threadIdx.x & (NN_T - 1);
+  const void* src = stage_q ? query : train;
+  const int64_t sn = stage_q ? nq : nt, sr = (stage_q ? q0 : t0) + srow;
+  double acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  NnRaw<KIND> raw;
+  nn_fetch<KIND>(src, sn, dim, sr, 0, raw);
+  __syncthreads();  // LUT in shared memory
+  nn_store<KIND>(raw, L, (stage_q ? As : Bs), srow, sr < sn, dim);
   __syncthreads();
+  int buf = 0;
   for (int64_t k0 = 0; k0 < dim; k0 += NN_K) {
-    nn_stage<KIND>(query, nq, dim, q0, k0, L, As);
-    nn_stage<KIND>(train, nt, dim, t0, k0, L, Bs);
-    __syncthreads();
-#pragma unroll 8
+    const bool more = k0 + NN_K < dim;
+    if (more) nn_fetch<KIND>(src, sn, dim, sr, k0 + NN_K, raw);  // next stage, in flight during the math
+    const double (*A)[NN_T + 2] = As + buf * NN_K;
+    const double (*B)[NN_T + 2] = Bs + buf * NN_K;
+#pragma unroll 4
     for (int k = 0; k < NN_K; ++k) {
-      double a[4], b[4];
+      double a[8], b[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[k][ty * 4 + i];
+      for (int i = 0; i < 4; ++i) {
+        const double2 va = *reinterpret_cast<const double2*>(&A[k][ty * 2 + 32 * i]);
+        const double2 vb = *reinterpret_cast<const double2*>(&B[k][tx * 2 + 32 * i]);
+        a[2 * i] = va.x;
+        a[2 * i + 1] = va.y;
+        b[2 * i] = vb.x;
+        b[2 * i + 1] = vb.y;
+      }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx * 4 + j];
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
     }
+    if (more) nn_store<KIND>(raw, L, (stage_q ? As : Bs) + (buf ^ 1) * NN_K, srow, sr < sn, dim - (k0 + NN_K));
     __syncthreads();
+    buf ^= 1;
   }
   // distances and the per-row candidate of this tile
+  NnCand* red = reinterpret_cast<NnCand*>(nn_sm);  // [NN_T][16], aliases the staging tiles
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t qi = q0 + ty * 4 + i;
+  for (int i = 0; i < 8; ++i) {
+    const int rl = ty * 2 + (i & 1) + 32 * (i >> 1);
+    const int64_t qi = q0 + rl;
     double bd = DBL_MAX;
     int64_t bl = INT64_MAX;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t tj = t0 + tx * 4 + j;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t tj = t0 + tx * 2 + (j & 1) + 32 * (j >> 1);
       if (qi >= nq || tj >= nt) continue;
       double d;
       if (metric == 0) {
@@ -133,18 +201,23 @@ __global__ void __launch_bounds__(NN_THREADS)
       const int64_t l = labels[tj];
       if (nn_better(d, l, bd, bl)) { bd = d; bl = l; }
     }
-    red_d[ty * 4 + i][tx] = bd;
-    red_l[ty * 4 + i][tx] = bl;
+    red[rl * 16 + tx] = {bd, bl};
   }
   __syncthreads();
   if (threadIdx.x < NN_T) {
     const int r = threadIdx.x;
     double bd = DBL_MAX;
     int64_t bl = INT64_MAX;
-    for (int c = 0; c < 16; ++c)
-      if (nn_better(red_d[r][c], red_l[r][c], bd, bl)) { bd = red_d[r][c]; bl = red_l[r][c]; }
+    for (int c = 0; c < 16; ++c) {
+      const NnCand x = red[r * 16 + c];
+      if (nn_better(x.dist, x.label, bd, bl)) { bd = x.dist; bl = x.label; }
+    }
     if (q0 + r < nq) cand[(q0 + r) * gridDim.x + blockIdx.x] = {bd, bl};
   }
+}
+
+static size_t nn_smem(int kind, int lut_len) {
+  return sizeof(double) * (4 * (size_t)NN_K * (NN_T + 2) + (kind == 0 ? (size_t)lut_len : 0));
 }
 
 __global__ void nn_reduce_kernel(const NnCand* __restrict__ cand, int64_t nq, int ntiles, int64_t* __restrict__ pred) {
@@ -194,8 +267,10 @@ static int nn_run(const void* q, int64_t nq, const void* t, int64_t nt, int64_t 
   const int ntiles = (int)((nt + NN_T - 1) / NN_T);
   const int64_t qtiles = (nq + NN_T - 1) / NN_T;
   if (qtiles > 65535) return fail(DDCCA_ECONFIG, "nn: %lld query rows exceed one launch", (long long)nq);
-  nn_tile_kernel<KIND><<<dim3(ntiles, (unsigned)qtiles), NN_THREADS, 0, st>>>(q, nq, t, nt, dim, lut, lut_len, qn,
-                                                                             tn, labels, metric, cand);
+  const size_t sm = nn_smem(KIND, lut_len);
+  cudaFuncSetAttribute(nn_tile_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  nn_tile_kernel<KIND><<<dim3(ntiles, (unsigned)qtiles), NN_THREADS, sm, st>>>(q, nq, t, nt, dim, lut, lut_len, qn,
+                                                                              tn, labels, metric, cand);
   DDCCA_TRY(check_launch("nn_tile"));
   nn_reduce_kernel<<<(int)std::min<int64_t>((nq + 255) / 256, 4096), 256, 0, st>>>(cand, nq, ntiles, pred);
   return check_launch("nn_reduce");
