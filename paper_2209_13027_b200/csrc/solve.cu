@@ -327,10 +327,13 @@ __device__ int inv_sqrt_dev(const double* c, int n, double* r, double* w, double
   int rc = sym_eig_dev(c, n, w, v, a, va, cs, tmp, wtmp, B);
   if (rc != DDCCA_OK) return rc;
   if (!(w[n - 1] > 0.0)) return DDCCA_ENUMERICAL;
+  // w^-1/2 once per eigenvalue (the same pow values the per-term form would use)
+  for (int k = threadIdx.x; k < n; k += blockDim.x) wtmp[k] = pow(w[k], -0.5);
+  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
     double s = 0.0;
-    for (int k = 0; k < n; ++k) s += (v[i * n + k] * pow(w[k], -0.5)) * v[j * n + k];
+    for (int k = 0; k < n; ++k) s += (v[i * n + k] * wtmp[k]) * v[j * n + k];
     tmp[e] = s;
   }
   __syncthreads();
