@@ -24,6 +24,10 @@
 namespace ddcca {
 
 constexpr int CC_THREADS = 256;
+// packed f32x2 FMAs in the tap loop (sm_100a): on for the fused last layer, where the
+// histogram phases compete for issue slots; the plain conv measured faster without
+constexpr bool CC_FFMA2_HIST = true;
+constexpr bool CC_FFMA2_CONV = false;
 // FFMAs per strip up to which the tap-row loop is unrolled. 0: always rolled. (Unrolling
 // does not turn the taps into immediate constant operands on sm_100a: the compiler
 // still stages them through uniform registers, at more LDCU per FFMA for short strips.)
@@ -64,7 +68,7 @@ __host__ __device__ inline int cc_buf_elems(int rows_in, int wt) { return (rows_
 // Each staged input row feeds the PY output rows it overlaps, so one row of x values
 // and one row of taps serve PY * PX * NF FFMAs.
 // Tile column v + SH holds padded column v.
-template <int L1, int L2, int NF, int PX, int PY, int SH>
+template <int L1, int L2, int NF, int PX, int PY, int SH, bool F2 = false>
 __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const float* __restrict__ tile, int Wt, int r0,
                                          int v0, bool center, float (&acc)[PY][PX][NF]) {
   const float c = center ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + SH + (L2 - 1) / 2] : 0.f;
@@ -94,13 +98,31 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
     for (int y = 0; y < PY; ++y) {
       const int ta = a - y;  // tap row of output row y that reads input row a
       if (ta >= 0 && ta < L1) {
+        if constexpr (NF % 2 == 0 && F2) {
+          // packed fma.rn.f32x2 over filter pairs (g, g+1): a warp-uniform weight pair, the
+          // broadcast x value, an accumulator pair -- half the issue slots, same per-lane
+          // rounding as two fmaf
 #pragma unroll
-        for (int b = 0; b < L2; ++b)
-#pragma unroll
-          for (int g = 0; g < NF; ++g)
+          for (int b = 0; b < L2; ++b)
 #pragma unroll
             for (int j = 0; j < PX; ++j)
-              acc[y][j][g] = fmaf(T.w[(ta * L2 + b) * NF + g], x[j + b], acc[y][j][g]);
+#pragma unroll
+              for (int g = 0; g < NF; g += 2) {
+                const float2 w2 = make_float2(T.w[(ta * L2 + b) * NF + g], T.w[(ta * L2 + b) * NF + g + 1]);
+                const float2 a2 = __ffma2_rn(w2, make_float2(x[j + b], x[j + b]),
+                                             make_float2(acc[y][j][g], acc[y][j][g + 1]));
+                acc[y][j][g] = a2.x;
+                acc[y][j][g + 1] = a2.y;
+              }
+        } else {
+#pragma unroll
+          for (int b = 0; b < L2; ++b)
+#pragma unroll
+            for (int g = 0; g < NF; ++g)
+#pragma unroll
+              for (int j = 0; j < PX; ++j)
+                acc[y][j][g] = fmaf(T.w[(ta * L2 + b) * NF + g], x[j + b], acc[y][j][g]);
+        }
       }
     }
   };
@@ -207,7 +229,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     if (r < rows_out && u0 + r < A.oh) {
       const int v0 = gi * PX;
       float acc[PY][PX][NF];
-      cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
+      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_CONV>(T, cur, Wt, r, v0, A.center, acc);
 #pragma unroll
       for (int y = 0; y < PY; ++y) {
         const int u = u0 + r + y;
@@ -278,7 +300,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += NT) {
       const int r = s / G * PY, v0 = (s % G) * PX;
       float acc[PY][PX][NF];
-      cc_strip<L1, L2, NF, PX, PY, SH>(T, cur, Wt, r, v0, A.center, acc);
+      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_HIST>(T, cur, Wt, r, v0, A.center, acc);
       const int bx0 = v0 / A.bw, rem0 = v0 - bx0 * A.bw;
       if (v0 + PX <= cols && rem0 + PX <= A.bw) {
         // whole strip inside one block: no per-pixel bounds or block stepping
