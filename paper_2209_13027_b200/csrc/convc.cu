@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     if (r < rows_out && u0 + r < A.oh) {
       const int v0 = gi * PX;
       float acc[PY][PX][NF];
-      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_CONV>(T, cur, Wt, r, v0, A.center, acc);
+      cc_strip<L1, L2, NF, PX, PY, SH, (CC_FFMA2_CONV || NF > 8)>(T, cur, Wt, r, v0, A.center, acc);
 #pragma unroll
       for (int y = 0; y < PY; ++y) {
         const int u = u0 + r + y;
