@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--deterministic", type=int, default=1)
+    ap.add_argument("--classify", action="store_true",
+                    help="also run the device NN classifier on the step's counts (accuracy, fp64 GEMM rate)")
     ap.add_argument("--moments", default="exact", choices=("exact", "blocked"),
                     help="lag-product precision of layers >= 2 (ExecSettings.moments)")
     return ap.parse_args()
@@ -274,6 +276,35 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         kern[name] = {"ms_avg": sum(times) / len(times), "launches": len(times),
                       "ms_per_step": sum(times) / args.steps, "work": w or None}
 
+    # optional downstream check: NN classifier on the step's device counts,
+    # half the images as training rows (every class on both sides), accuracy + fp64 GEMM rate
+    downstream = None
+    if args.classify and world == 1 and counts_buf[0] is not None:
+        cls_of = np.arange(s1 - s0) // classes % 2 == 0
+        tr_idx = torch.from_numpy(np.nonzero(cls_of)[0]).to(dev)
+        te_idx = torch.from_numpy(np.nonzero(~cls_of)[0]).to(dev)
+        lab_h = lab.astype(np.int64)
+        with torch.cuda.stream(ex.stream):
+            ctr = counts_buf[0].index_select(0, tr_idx)
+            cte = counts_buf[0].index_select(0, te_idx)
+        model = P.classify.fit(P.CountFeatures(ctr, plan, enc), lab_h[cls_of], executor=ex)
+        ex.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(ex.stream)
+        rep = P.classify.evaluate(model, P.CountFeatures(cte, plan, enc), lab_h[~cls_of], executor=ex)
+        b.record(ex.stream)
+        b.synchronize()
+        t_ms = a.elapsed_time(b)
+        flop = 2.0 * int(cls_of.sum()) * int((~cls_of).sum()) * featlen
+        sm_mhz = (clocks.get("sm_mhz") or 1965.0)
+        peak64 = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+        downstream = {"classifier": "nearest_neighbor euclidean on device counts (classify.py:109-143)",
+                      "train": int(cls_of.sum()), "test": int((~cls_of).sum()), "accuracy": rep.accuracy,
+                      "ms": t_ms, "tflops_fp64": flop / (t_ms / 1e3) / 1e12, "peak_fp64_tflops": peak64,
+                      "frac": flop / (t_ms / 1e3) / 1e12 / peak64}
+        del ctr, cte, model
+
     # e2e through the public API with host buffers
     e2e = None
     eng.maps_cache = None
@@ -390,6 +421,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "counts_output": "streamed+digested per super-batch" if stream_counts else "kept in HBM",
                    "deterministic": bool(args.deterministic)},
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "gram": gram,
+        "downstream": downstream,
         "kernels": kern, "peaks_source": pk_kind,
     }
     print(json.dumps(line), flush=True)
