@@ -395,7 +395,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             roof["kernel"], "lag_tma_kernel" if roof["kernel"].startswith("moments") else roof["kernel"])
         if tf.exists():
             t = json.loads(tf.read_text())
-            k = t.get("kernels", {}).get(kname)
+            k = t.get("kernels", {}).get(kname) if t.get("workload", "caltech256") == args.workload else None
             if k:
                 roof["traffic"] = k["dram_bytes_per_launch"]
                 roof["traffic_unit"] = "bytes/launch (dram read+write)"

@@ -4,7 +4,7 @@ Per kernel: launches, average DRAM bytes (read + write) per launch and average
 cold/serialized duration. bench.py reads this file to fill roofline.traffic
 for the dominant kernel (the bytes a real launch moved, against the
 algorithmic bytes it reports as `achieved`).
-Usage: python tools/traffic_from_ncu.py gpurun_out/prof_round/launches.csv profiles/traffic.json <label>
+Usage: python tools/traffic_from_ncu.py gpurun_out/prof_round/launches.csv profiles/traffic.json <label> [workload]
 """
 import csv
 import json
@@ -15,7 +15,7 @@ UNIT = {"byte": 1.0, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 
         "nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}
 
 
-def main(src, dst, label):
+def main(src, dst, label, workload="caltech256"):
     rows = list(csv.reader(open(src)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
@@ -28,7 +28,7 @@ def main(src, dst, label):
         name = r[ki].split("(")[0].replace("void ", "").replace("ddcca::", "").split("<")[0]
         agg[name][r[mi]] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         ids[name].add(r[idi])
-    out = {"source": label, "kernels": {}}
+    out = {"source": label, "workload": workload, "kernels": {}}
     for name, a in agg.items():
         n = len(ids[name])
         out["kernels"][name] = {
@@ -40,4 +40,4 @@ def main(src, dst, label):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
