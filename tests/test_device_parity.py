@@ -486,3 +486,29 @@ def test_blocked_moments_close_to_exact(ex, l, p, q):
         err = np.linalg.norm(a[:, lo:hi] - b[:, lo:hi]) / np.linalg.norm(a[:, lo:hi])
         assert 0 < err <= 1e-7, err  # nonzero: the float32 path really ran
     assert np.array_equal(a[:, 2 * d * d:], b[:, 2 * d * d:])  # sums / counts stay exact
+
+
+@pytest.mark.parametrize("m,p,q,batch,l,blk", [(1, 12, 10, 8, 3, (4, 4)), (37, 9, 11, 16, 5, (3, 4)),
+                                                (130, 16, 12, 128, 3, (5, 5)), (20, 6, 6, 8, 7, (2, 3))])
+def test_edge_shapes_vs_oracle(ex, m, p, q, batch, l, blk):
+    """Single sample, ragged last batch, maps smaller than the window: statistics, filters and features."""
+    rng = np.random.default_rng(m + p)
+    v1 = rng.uniform(size=(m, p, q)).astype(np.float32)
+    v2 = rng.uniform(size=(m, p, q)).astype(np.float32)
+    lab = np.arange(m) % 3 if m >= 3 else np.zeros(m, dtype=np.int64)
+    classes = int(lab.max()) + 1
+    ds = P.ViewPairDataset.from_arrays(v1, v2, lab, class_count=classes)
+    geom = P.PatchGeometry(l, l)
+    net = P.NetworkConfig((P.LayerConfig(3, geom), P.LayerConfig(2, geom)), batch=P.BatchSpec(batch))
+    specs = [(3, O.Geometry(l, l), True), (2, O.Geometry(l, l), True)]
+    ref_layers, stats = O.train(v1.astype(np.float64), v2.astype(np.float64), lab, classes, specs, batch=batch,
+                                return_stats=True)
+    with torch.cuda.stream(ex.stream):
+        acc = P.accumulate_layer_moments(P.layer_input(ds), geom, True, classes, net.batch, ex)
+    assert rel(acc.c11, stats[0][0].c11) <= 1e-11 and rel(acc.c22, stats[0][0].c22) <= 1e-11
+    bank = P.train_network(ds, net, ex)
+    cfg = type("Cfg", (), {"net": net, "encoder": P.EncoderConfig(*blk)})()
+    got = P.compute_features(ds, bank, cfg, ex)
+    want = O.features(v1, v2, _oracle_layers(bank), O.EncodeCfg(*blk), batch=batch)
+    assert got.shape == want.shape
+    assert np.mean(got == want) >= 0.999
