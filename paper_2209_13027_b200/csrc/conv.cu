@@ -469,7 +469,7 @@ static int launch_conv(const ConvArgs& A, int stride, cudaStream_t st) {
 
 static int conv_args(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* pack, int count, int center,
                      void* out, ConvArgs* A, int* stride) {
-  Geo g;
+  Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (count < 1 || count > g.d) return fail(DDCCA_ECONFIG, "filter count %d outside [1, %d]", count, g.d);
   if (n_maps < 0) return fail(DDCCA_ESHAPE, "negative map count");
@@ -489,7 +489,7 @@ extern "C" {
 int ddcca_conv(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack, int count, int center,
                float* out, void* stream) {
   ConvArgs A;
-  int stride;
+  int stride = 1;
   DDCCA_TRY(conv_args(in, n_maps, g, conv_pack, count, center, out, &A, &stride));
   if (count > 64) return fail(DDCCA_ECONFIG, "conv: at most 64 filters per layer on device");
   return launch_conv<0>(A, stride, as_stream(stream));
@@ -498,7 +498,7 @@ int ddcca_conv(const float* in, int64_t n_maps, const ddcca_geom* g, const float
 int ddcca_conv_hash(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack, int count,
                     int center, void* codes, void* stream) {
   ConvArgs A;
-  int stride;
+  int stride = 1;
   DDCCA_TRY(conv_args(in, n_maps, g, conv_pack, count, center, codes, &A, &stride));
   if (count > 16) return fail(DDCCA_ECONFIG, "hash width %d above the device limit of 16 bits", count);
   if (count <= 8) return launch_conv<1>(A, stride, as_stream(stream));
@@ -554,7 +554,7 @@ int ddcca_sign_hash(const float* maps, int64_t n_groups, int n_bits, int64_t pla
 }
 
 int ddcca_im2col(const double* maps, int64_t n_maps, const ddcca_geom* gg, int center, double* out, void* stream) {
-  Geo g;
+  Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   const int64_t cols = n_maps * (int64_t)g.oh * g.ow;
   if (cols == 0) return DDCCA_OK;

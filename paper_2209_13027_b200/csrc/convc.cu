@@ -535,7 +535,7 @@ extern "C" {
 
 int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
                   int center, float* out, void* stream) {
-  Geo g;
+  Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (g.stride != 1) return fail(DDCCA_ECONFIG, "constant-bank conv needs stride 1");
   if (count < 1 || count > g.d) return fail(DDCCA_ECONFIG, "filter count %d outside [1, %d]", count, g.d);
@@ -550,7 +550,7 @@ int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const f
 int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
                        int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,
                        int64_t row_stride, int64_t group_stride, void* stream) {
-  Geo g;
+  Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (g.stride != 1) return fail(DDCCA_ECONFIG, "fused conv-histogram needs stride 1");
   if (count < 1 || count > 16) return fail(DDCCA_ECONFIG, "hash width %d outside the fused path (1..16)", count);

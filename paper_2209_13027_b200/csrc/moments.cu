@@ -87,7 +87,7 @@ struct RecInfo {
 };
 
 struct Plan {
-  Geo g;
+  Geo g{};
   Zones z;
   int nrz, ncz, G, NDX, NDF, slab;
   std::vector<Task> tasks;
@@ -1113,7 +1113,7 @@ int64_t ddcca_payload_len(int dim, int class_count) { return payload_len(dim, cl
 
 size_t ddcca_moments_workspace(const ddcca_geom* gg, int n_batches, int64_t max_maps_per_batch, int class_count) {
   (void)class_count;
-  Geo g;
+  Geo g{};
   if (make_geo(gg, &g) != DDCCA_OK) return 0;
   // worst case over the per-batch maps: n_maps <= n_batches * max_maps
   const int64_t n_maps = (int64_t)n_batches * max_maps_per_batch;
@@ -1139,7 +1139,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
                              int class_count, double* partials, void* ws, size_t ws_bytes, int flags,
                              void* stream) {
   if (flags & ~DDCCA_MOMENTS_F32_BLOCKS) return fail(DDCCA_ECONFIG, "unknown moments flags 0x%x", flags);
-  Geo g;
+  Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (n_batches < 1) return fail(DDCCA_ECONFIG, "no batches to accumulate");
   if (class_count < 1) return fail(DDCCA_ECONFIG, "invalid class count %d", class_count);
