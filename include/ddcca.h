@@ -228,6 +228,12 @@ DDCCA_API int ddcca_nn_classify(const void* query, int64_t n_query, const void* 
                                 int64_t dim, int row_kind, const double* lut, int lut_len,
                                 const int64_t* train_labels, int metric, int64_t* pred, void* workspace,
                                 size_t ws_bytes, void* stream);
+/* Linear one-vs-all prediction (ridge models, classify.py:140-142): pred[i] =
+ * the class of the largest x_i . w_c + bias_c, lowest class id on ties
+ * (class_ids[c] per weight row). Float64 rows; workspace ddcca_nn_workspace(nq, n_class). */
+DDCCA_API int ddcca_linear_classify(const double* query, int64_t n_query, const double* weights, int64_t n_class,
+                                    int64_t dim, const double* bias, const int64_t* class_ids, int64_t* pred,
+                                    void* workspace, size_t ws_bytes, void* stream);
 /* Saturating-u8 block counts (count_kind 1) -> exact u16 counts. */
 DDCCA_API int ddcca_counts_to_u16(const uint8_t* counts, int64_t n_blocks, int bins, int bpc, uint16_t* out,
                                   void* stream);

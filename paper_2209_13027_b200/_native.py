@@ -57,6 +57,7 @@ _SIGNATURES = {
     "ddcca_nn_workspace": (_sz, [_i64, _i64]),
     "ddcca_nn_classify": (_i32, [_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _i32, _vp, _vp, _sz, _vp]),
     "ddcca_counts_to_u16": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
+    "ddcca_linear_classify": (_i32, [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ddcca_lbp": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "ddcca_pgm_info": (_i32, [C.c_char_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i64)]),
     "ddcca_pgm_load_many": (_i32, [C.POINTER(C.c_char_p), _i64, _i32, _i32, _vp, _i32]),

@@ -11,9 +11,10 @@ the epilogue, so the distance matrix never exists. Rows are float64 features
 counts ``compute_feature_counts`` leaves in HBM (``CountFeatures``), expanded
 through the IQ LUT inside the kernel's tile staging.
 
-``ridge_one_vs_all`` needs a dense (n x n) or (d x d) eigen-solve of the Gram
-that is not on this path; it raises ``ConfigError`` (SURVEY 8(f) ranks the NN
-classifier as the next row, not ridge).
+``ridge_one_vs_all``: fitting needs a dense (n x n) or (d x d) eigen-solve of
+the Gram that is not on this path and raises ``ConfigError``; prediction with
+a trained (e.g. loaded) ridge model runs on the device through the same tiled
+GEMM (``ddcca_linear_classify``: largest [x, 1] . w_c, lowest class on ties).
 """
 
 from __future__ import annotations
@@ -148,7 +149,7 @@ def predict_many(model: ClassifierModel, features, executor=None) -> np.ndarray:
 
     ex = _executor(executor)
     if model.kind != "nearest_neighbor":
-        raise ConfigError("ridge_one_vs_all prediction is not on the device path (nearest_neighbor only)")
+        return _predict_linear(ex, model, features)
     if not hasattr(model.train_features, "data_ptr"):  # e.g. a loaded model: float64 rows on the host
         rows, model.row_kind, model.lut = _rows(ex, model.train_features)
         model.train_features = rows
@@ -172,6 +173,35 @@ def predict_many(model: ClassifierModel, features, executor=None) -> np.ndarray:
             ws_bytes, _native.stream_ptr(ex.stream)), "nn_classify")
         out = pred.cpu().numpy()
     return out
+
+
+def _predict_linear(ex, model: ClassifierModel, features) -> np.ndarray:
+    """Ridge one-vs-all scores [x, 1] . w_c, argmax with the lowest class on ties (classify.py:140-142)."""
+    import torch
+
+    from . import engine as E
+
+    w = np.asarray(model.weights, dtype=np.float64)
+    if isinstance(features, CountFeatures):
+        with torch.cuda.stream(ex.stream):
+            q = E.Engine(ex).expand(features.counts, features.plan, features.encoder)
+    else:
+        q, _, _ = _rows(ex, features)
+    if q.ndim != 2 or q.shape[1] != w.shape[1] - 1:
+        raise ShapeError(f"feature dim {q.shape[-1]} does not match model dim {w.shape[1] - 1}")
+    lib = _native.load()
+    nq, nc, dim = q.shape[0], w.shape[0], w.shape[1] - 1
+    with torch.cuda.stream(ex.stream):
+        wd = torch.from_numpy(np.ascontiguousarray(w[:, :dim])).to(ex.device)
+        bd = torch.from_numpy(np.ascontiguousarray(w[:, dim])).to(ex.device)
+        ids = torch.arange(nc, dtype=torch.int64, device=ex.device)
+        pred = torch.empty(nq, dtype=torch.int64, device=ex.device)
+        ws_bytes = lib.ddcca_nn_workspace(nq, nc)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=ex.device)
+        _native.check(lib.ddcca_linear_classify(_native.ptr(q), nq, _native.ptr(wd), nc, dim, _native.ptr(bd),
+                                                _native.ptr(ids), _native.ptr(pred), _native.ptr(ws), ws_bytes,
+                                                _native.stream_ptr(ex.stream)), "linear_classify")
+        return pred.cpu().numpy()
 
 
 def predict(model: ClassifierModel, feature, executor=None) -> int:

@@ -194,6 +194,8 @@ __global__ void __launch_bounds__(NN_THREADS, 1)
       double d;
       if (metric == 0) {
         d = (qn[qi] + tn[tj]) - 2.0 * acc[i][j];
+      } else if (metric == 2) {
+        d = -(acc[i][j] + tn[tj]);  // linear scores (ridge): tn = bias, best = largest score
       } else {
         const double den = qn[qi] * tn[tj];
         d = 1.0 - (den > 0.0 ? acc[i][j] / den : 0.0);
@@ -255,14 +257,19 @@ static size_t nn_cand_bytes(int64_t nq, int64_t nt) {
 
 template <int KIND>
 static int nn_run(const void* q, int64_t nq, const void* t, int64_t nt, int64_t dim, const double* lut, int lut_len,
-                  const int64_t* labels, int metric, int64_t* pred, void* ws, cudaStream_t st) {
+                  const int64_t* labels, int metric, int64_t* pred, void* ws, cudaStream_t st,
+                  const double* bias = nullptr) {
   double* qn = static_cast<double*>(ws);
   double* tn = qn + nq;
   NnCand* cand = reinterpret_cast<NnCand*>(tn + nt + (((nq + nt) & 1) ? 1 : 0));
   const size_t lsm = KIND == 3 ? 0 : sizeof(double) * (size_t)lut_len;
   const int nb = (int)std::min<int64_t>((std::max(nq, nt) + 7) / 8, 148 * 8);
-  nn_norms_kernel<KIND><<<nb, 256, lsm, st>>>(q, nq, dim, lut, lut_len, metric == 1, qn);
-  nn_norms_kernel<KIND><<<nb, 256, lsm, st>>>(t, nt, dim, lut, lut_len, metric == 1, tn);
+  if (metric == 2) {
+    cudaMemcpyAsync(tn, bias, sizeof(double) * nt, cudaMemcpyDeviceToDevice, st);
+  } else {
+    nn_norms_kernel<KIND><<<nb, 256, lsm, st>>>(q, nq, dim, lut, lut_len, metric == 1, qn);
+    nn_norms_kernel<KIND><<<nb, 256, lsm, st>>>(t, nt, dim, lut, lut_len, metric == 1, tn);
+  }
   DDCCA_TRY(check_launch("nn_norms"));
   const int ntiles = (int)((nt + NN_T - 1) / NN_T);
   const int64_t qtiles = (nq + NN_T - 1) / NN_T;
@@ -306,6 +313,20 @@ int ddcca_nn_classify(const void* query, int64_t n_query, const void* train, int
     default:
       return fail(DDCCA_ECONFIG, "nn: row kind %d not u8(0)/u16(2)/f64(3)", row_kind);
   }
+}
+
+// Linear one-vs-all prediction (classify.py:140-142): pred = argmax_c (x . w_c + b_c), the
+// first maximum on ties -> the lowest class id, as (-score, class) minima through the same
+// tiled float64 GEMM. query (nq x dim) and weights (n_class x dim) are float64 rows.
+int ddcca_linear_classify(const double* query, int64_t n_query, const double* weights, int64_t n_class, int64_t dim,
+                          const double* bias, const int64_t* class_ids, int64_t* pred, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  if (n_query < 0 || n_class < 1 || dim < 1) return fail(DDCCA_ESHAPE, "linear: empty weights or feature dim");
+  if (!weights || !bias || !class_ids) return fail(DDCCA_ESHAPE, "linear: null pointer");
+  if (n_query == 0) return DDCCA_OK;
+  if (ws_bytes < ddcca_nn_workspace(n_query, n_class)) return fail(DDCCA_ESHAPE, "linear: workspace too small");
+  return nn_run<3>(query, n_query, weights, n_class, dim, nullptr, 0, class_ids, 2, pred, workspace, as_stream(stream),
+                   bias);
 }
 
 int ddcca_counts_to_u16(const uint8_t* counts, int64_t n_blocks, int bins, int bpc, uint16_t* out, void* stream) {

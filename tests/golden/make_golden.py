@@ -286,6 +286,13 @@ def make_models(dd):
                  OUT / "model_nn.txt")
     ridge = Cl.fit(feats[:, :20], labels, kind="ridge_one_vs_all")
     M.save_model(M.ModelArtifact(snapshot=snap, bank=bank, classifier=ridge), OUT / "model_ridge.txt")
+    # reference predictions of the ridge model, and of a model with tied class scores
+    rng = np.random.default_rng(3)
+    q = np.concatenate([feats[:, :20], rng.standard_normal((10, 20))])
+    tied = Cl.ClassifierModel(kind="ridge_one_vs_all", class_count=3, lam=1.0,
+                              weights=np.stack([ridge.weights[1], ridge.weights[1], ridge.weights[0]]))
+    np.savez_compressed(OUT / "ridge.npz", queries=q, pred=Cl.predict_many(ridge, q),
+                        tied_weights=tied.weights, tied_pred=Cl.predict_many(tied, q))
 
 
 if __name__ == "__main__":

@@ -68,3 +68,16 @@ def test_device_model_save_load_predict(tmp_path):
     assert np.array_equal(back.classifier.train_features, feats)  # count rows written as their IQ values
     assert np.array_equal(P.classify.predict_many(back.classifier, feats, ex),
                           P.classify.predict_many(clf, P.CountFeatures(counts, plan, enc), ex))
+
+
+@pytest.mark.gpu
+def test_ridge_model_predictions_match_reference(golden):
+    """Loaded ridge model -> ddcca_linear_classify == the reference's predict_many, incl. tied class scores."""
+    import paper_2209_13027_b200 as P
+    from paper_2209_13027_b200 import model_io as M
+
+    g = golden("ridge")
+    art = M.load_model(GOLDEN / "model_ridge.txt")
+    assert np.array_equal(P.classify.predict_many(art.classifier, g["queries"]), g["pred"])
+    tied = P.ClassifierModel(kind="ridge_one_vs_all", class_count=3, lam=1.0, weights=g["tied_weights"])
+    assert np.array_equal(P.classify.predict_many(tied, g["queries"]), g["tied_pred"])
