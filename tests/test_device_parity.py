@@ -512,3 +512,40 @@ def test_edge_shapes_vs_oracle(ex, m, p, q, batch, l, blk):
     want = O.features(v1, v2, _oracle_layers(bank), O.EncodeCfg(*blk), batch=batch)
     assert got.shape == want.shape
     assert np.mean(got == want) >= 0.999
+
+
+def test_caltech_shaped_subsample_vs_oracle(ex):
+    """parity on a Caltech-shaped subsample (128 x 128 images, 7 x 7, 8 filters, 16 x 16 blocks,
+    257 classes, one 128-sample batch): layer-1 statistics and well-posed filters vs the oracle, and the
+    transform of 8 images with the device bank vs the oracle's encode of the same bank."""
+    cfg = synthetic.CONFIGS["caltech256"]
+    m = 128
+    v1, lab = synthetic.blob_images(m, cfg["p"], cfg["q"], cfg["classes"], seed=0)
+    v2 = synthetic.second_view(v1, lab, cfg["view2"], cfg["classes"], seed=1)
+    v1, v2 = v1.astype(np.float32), v2.astype(np.float32)
+    classes = cfg["classes"]
+    geom = P.PatchGeometry(7, 7)
+    net = P.NetworkConfig((P.LayerConfig(8, geom), P.LayerConfig(8, geom)), batch=P.BatchSpec(128))
+    ds = P.ViewPairDataset.from_arrays(v1, v2, lab, class_count=classes)
+    with torch.cuda.stream(ex.stream):
+        acc = P.accumulate_layer_moments(P.layer_input(ds), geom, True, classes, net.batch, ex)
+    ref_layers, stats = O.train(v1.astype(np.float64), v2.astype(np.float64), lab, classes,
+                                [(8, O.Geometry(7, 7), True)], batch=128, return_stats=True)
+    ref = stats[0][0]
+    assert rel(acc.c11, ref.c11) <= 1e-11 and rel(acc.c22, ref.c22) <= 1e-11
+    assert rel(acc.class_sum1, ref.s1) <= 1e-11 and rel(acc.class_sum2, ref.s2) <= 1e-11
+    bank = P.train_network(ds, net, ex)
+    rho = O.dcca_solve(stats[0][1], 8).rho
+    lam = rho ** 2
+    for j in range(8):
+        gaps = [abs(lam[j] - lam[k]) for k in range(8) if k != j]
+        if min(gaps) <= 1e-6 * lam[0] or rho[j] <= 1e-10 * rho[0]:
+            continue
+        a, b = bank.layers[0].filters1[j], ref_layers[0].f1[j]
+        assert abs((a * b).sum()) / (np.linalg.norm(a) * np.linalg.norm(b)) >= 0.9999, j
+    sub = P.ViewPairDataset.from_arrays(v1[:8], v2[:8], lab[:8], class_count=classes)
+    pcfg = type("Cfg", (), {"net": net, "encoder": P.EncoderConfig(16, 16)})()
+    got = P.compute_features(sub, bank, pcfg, ex)
+    want = O.features(v1[:8], v2[:8], _oracle_layers(bank), O.EncodeCfg(16, 16), batch=8)
+    assert got.shape == want.shape == (8, 262144)
+    assert np.mean(got == want) >= 0.999
