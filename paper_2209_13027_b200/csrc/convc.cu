@@ -441,8 +441,10 @@ static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
   zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
   const int cols = A.nbx * A.bw;
   const int G = (cols + PX - 1) / PX;
-  // block rows per CTA: about one strip per thread, at least one block row
-  A.br = std::max(1, std::min(A.nby, PY * NT / std::max(1, A.bh * G)));
+  // block rows per CTA: about one strip per thread, two when a block row alone fills at
+  // least half the CTA (amortizes the per-tile staging, barriers and count output)
+  const int strips_br = std::max(1, A.bh * G);
+  A.br = std::max(1, std::min(A.nby, (strips_br * 2 >= NT ? 2 : 1) * PY * NT / strips_br));
   const int rows_out = A.br * A.bh;
   const int Wt = cc_tile_width(cols, L2, PX, SH);
   const int rows_in = (rows_out + PY - 1) / PY * PY + L1 - 1;
