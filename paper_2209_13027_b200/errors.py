@@ -18,33 +18,18 @@ class DdccanetError(Exception):
     """Root of every error this package raises."""
 
 
-class ParseError(DdccanetError):
-    """Input text or file content could not be parsed."""
+def _derive(name: str, doc: str) -> type:
+    """A direct DdccanetError subclass, defined in this module (picklable, catchable by name)."""
+    return type(name, (DdccanetError,), {"__doc__": doc, "__module__": __name__, "__qualname__": name})
 
 
-class IoError(DdccanetError):
-    """A file could not be found or read."""
-
-
-class ShapeError(DdccanetError):
-    """Array shapes / dimensions do not fit the operation (also: labels out of range)."""
-
-
-class EmptyDatasetError(DdccanetError):
-    """No samples were provided."""
-
-
-class ConfigError(DdccanetError):
-    """A configuration value is invalid or inconsistent."""
-
-
-class RecipeError(DdccanetError):
-    """Second-view construction does not match the raw planes."""
-
-
-class NumericalError(DdccanetError):
-    """Numerical breakdown: empty statistics, indefinite matrix, Jacobi non-convergence."""
-
-
-class CorruptModelError(DdccanetError):
-    """A stored model failed validation."""
+# (name, meaning) of every concrete error, in the reference's order
+ParseError = _derive("ParseError", "Input text or file content could not be parsed.")
+IoError = _derive("IoError", "A file could not be found or read.")
+ShapeError = _derive("ShapeError", "Array shapes / dimensions do not fit the operation (also: labels out of range).")
+EmptyDatasetError = _derive("EmptyDatasetError", "No samples were provided.")
+ConfigError = _derive("ConfigError", "A configuration value is invalid or inconsistent.")
+RecipeError = _derive("RecipeError", "Second-view construction does not match the raw planes.")
+NumericalError = _derive("NumericalError",
+                         "Numerical breakdown: empty statistics, indefinite matrix, Jacobi non-convergence.")
+CorruptModelError = _derive("CorruptModelError", "A stored model failed validation.")
