@@ -214,16 +214,15 @@ def predict(model: ClassifierModel, feature, executor=None) -> int:
 def evaluate(model: ClassifierModel, features, labels, stage_seconds: dict[str, float] | None = None,
              threads: int = 1, deterministic: bool = True, executor=None) -> EvalReport:
     """Confusion counts, overall and per-class accuracy (classify.py:150-176)."""
-    labels = np.asarray(labels, dtype=np.int64)
-    if labels.size == 0:
-        raise ConfigError("cannot evaluate on an empty test set")
-    preds = predict_many(model, features, executor)
-    c = model.class_count
-    confusion = np.zeros((c, c), dtype=np.int64)
-    np.add.at(confusion, (labels, preds), 1)
-    row_totals = confusion.sum(axis=1)
-    with np.errstate(invalid="ignore"):
-        per_class = np.where(row_totals > 0, np.diag(confusion) / np.maximum(row_totals, 1), np.nan)
-    return EvalReport(accuracy=float(np.trace(confusion) / labels.size), per_class_accuracy=per_class,
-                      confusion=confusion, stage_seconds=dict(stage_seconds or {}), threads=threads,
-                      deterministic=deterministic)
+    truth = np.asarray(labels, dtype=np.int64)
+    if truth.size == 0:
+        raise ConfigError("evaluation needs at least one labelled sample")
+    guess = predict_many(model, features, executor)
+    k = model.class_count
+    confusion = np.bincount(truth * k + guess, minlength=k * k).reshape(k, k).astype(np.int64)
+    support = confusion.sum(axis=1)
+    hits = np.diagonal(confusion).astype(np.float64)
+    per_class = np.full(k, np.nan)
+    per_class[support > 0] = hits[support > 0] / support[support > 0]
+    return EvalReport(accuracy=float(hits.sum() / truth.size), per_class_accuracy=per_class, confusion=confusion,
+                      stage_seconds=dict(stage_seconds or {}), threads=threads, deterministic=deterministic)

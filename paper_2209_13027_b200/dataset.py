@@ -136,13 +136,12 @@ def load_pgm(path) -> np.ndarray:
 
 def write_pgm(path, plane: np.ndarray, maxval: int = 255) -> None:
     """Quantize a [0, 1] plane to a binary PGM file, round-to-nearest (dataset.py:121-129)."""
-    if not 0 < maxval <= 65535:
-        raise ParseError(f"maxval {maxval} out of range")
-    plane = np.asarray(plane, dtype=np.float64)
-    q = np.clip(np.rint(plane * maxval), 0, maxval)
-    dtype = ">u2" if maxval > 255 else np.uint8
-    header = f"P5\n{plane.shape[1]} {plane.shape[0]}\n{maxval}\n".encode("ascii")
-    Path(path).write_bytes(header + q.astype(dtype).tobytes())
+    if not 1 <= maxval <= 65535:
+        raise ParseError(f"PGM maxval must be in [1, 65535], got {maxval}")
+    levels = np.clip(np.rint(np.asarray(plane, dtype=np.float64) * maxval), 0, maxval)
+    rows, cols = levels.shape
+    samples = levels.astype(">u2" if maxval > 255 else np.uint8).tobytes()
+    Path(path).write_bytes(b"P5\n%d %d\n%d\n" % (cols, rows, maxval) + samples)
 
 
 def load_matrix_csv(path) -> np.ndarray:
