@@ -16,7 +16,7 @@
 
 namespace ddcca {
 
-constexpr int SOLVE_THREADS = 512;  // latency-bound rounds: more warps per rotation pass
+constexpr int SOLVE_THREADS = 1024;  // latency-bound rounds: more warps per rotation pass
 
 #ifdef DDCCA_SOLVE_PROF  // diagnostic build only (tools/microbench/jacobi_probe.cu)
 __device__ unsigned long long g_solve_prof[8];
