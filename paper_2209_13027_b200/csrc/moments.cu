@@ -1187,12 +1187,17 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
     zones.insert(zones.end(), P.z.cz_hi.begin(), P.z.cz_hi.end());
     zones.insert(zones.end(), P.z.rz_of_y.begin(), P.z.rz_of_y.end());
     zones.insert(zones.end(), P.z.cz_of_x.begin(), P.z.cz_of_x.end());
-    cudaMemcpyAsync(w + L.off_tasks, td.data(), sizeof(TaskDev) * td.size(), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(w + L.off_lane, P.lane_slot.data(), sizeof(int) * P.lane_slot.size(), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(w + L.off_boff, batch_offsets_host, sizeof(int64_t) * (n_batches + 1), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(w + L.off_zoff, zoff.data(), sizeof(int) * zoff.size(), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(w + L.off_zlist, zlist.data(), sizeof(int) * zlist.size(), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(w + L.off_zones, zones.data(), sizeof(int) * zones.size(), cudaMemcpyHostToDevice, st);
+    {
+      const Upload parts[] = {
+          {td.data(), sizeof(TaskDev) * td.size(), w + L.off_tasks},
+          {P.lane_slot.data(), sizeof(int) * P.lane_slot.size(), w + L.off_lane},
+          {batch_offsets_host, sizeof(int64_t) * (n_batches + 1), w + L.off_boff},
+          {zoff.data(), sizeof(int) * zoff.size(), w + L.off_zoff},
+          {zlist.data(), sizeof(int) * zlist.size(), w + L.off_zlist},
+          {zones.data(), sizeof(int) * zones.size(), w + L.off_zones},
+      };
+      DDCCA_TRY(staged_upload(parts, 6, st));
+    }
     DDCCA_TRY(check_launch("moments: plan upload"));
     const int* zd = reinterpret_cast<const int*>(w + L.off_zones);
     const int *rz_lo = zd, *rz_hi = zd + P.nrz, *cz_lo = zd + 2 * P.nrz, *cz_hi = zd + 2 * P.nrz + P.ncz;
@@ -1259,7 +1264,10 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
         int* ids_dev = reinterpret_cast<int*>(w + L.off_ids);
         std::vector<int> ids_all(ids_int);
         ids_all.insert(ids_all.end(), ids_short.begin(), ids_short.end());
-        cudaMemcpyAsync(ids_dev, ids_all.data(), sizeof(int) * ids_all.size(), cudaMemcpyHostToDevice, st);
+        {
+          const Upload ids_part{ids_all.data(), sizeof(int) * ids_all.size(), ids_dev};
+          DDCCA_TRY(staged_upload(&ids_part, 1, st));
+        }
         auto tgo = [&](auto kern) {
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
           cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1343,7 +1351,10 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
   double* rec = reinterpret_cast<double*>(w + o_rec);
   int64_t* boff = reinterpret_cast<int64_t*>(w + o_boff);
   double* msum = reinterpret_cast<double*>(w + o_msum);
-  cudaMemcpyAsync(boff, batch_offsets_host, sizeof(int64_t) * (n_batches + 1), cudaMemcpyHostToDevice, st);
+  {
+    const Upload boff_part{batch_offsets_host, sizeof(int64_t) * (n_batches + 1), boff};
+    DDCCA_TRY(staged_upload(&boff_part, 1, st));
+  }
   const size_t sm = sizeof(double) * DIRECT_K * g.d;
   cudaFuncSetAttribute(direct_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   direct_gram_kernel<<<dim3(nsplit, n_batches, 2), 256, sm, st>>>(maps1, maps2, boff, g, center, nsplit, rec);
