@@ -707,20 +707,28 @@ __global__ void assemble_kernel(AsmArgs A) {
 struct RectArgs {
   const float* maps[2];
   double* out;  // [view][map][d]
-  const int* rz_of_y; const int* cz_of_x;
-  const int* rz_lo; const int* rz_hi; const int* cz_lo; const int* cz_hi;
+  const int* rz_y0;  // [nrz + 1] first padded row of each row zone, then Hp
+  const int* cz_of_x;
+  const int* a_rz;   // [l1][2] first / last row zone covering tap row a
+  const int* b_cz;   // [l2][2] first / last column zone covering tap column b
   int64_t n_maps;
   int p, q, top, left, Hp, Wp, nrz, ncz, l1, l2, d, center, big_cz;
 };
 
-// Warp per map. Rows are walked zone by zone; every lane keeps the running sums of
-// its own columns (float4 groups), which at a zone boundary go either to the
-// column's singleton zone (border columns) or into the warp-reduced interior
-// zone. Then R[a][b] = sum of the zone sums covering (a, b), centered.
+// Warp per map. Every lane keeps the running sums of its own columns (float4 groups)
+// over the rows of the current row zone; at a zone boundary (warp-uniform) the sums go
+// either to the column's singleton zone (border columns) or into the warp-reduced
+// interior zone. Rows stream in 8-row groups whatever the zones (the boundaries come
+// from the rz_y0 table, no per-row lookups). Then R[a][b] = sum of the zone sums
+// covering (a, b) (a contiguous zone range per a and per b), centered.
 constexpr int RS_WARPS = 4;
 constexpr int RS_COLS = 8;  // columns per lane (q <= 256)
+constexpr int RS_ROWS = 8;  // rows in flight per warp (narrow form)
 
+// NARROW: q % 4 == 0 and q <= 128 (one float4 per lane per row, 4 lane sums).
+template <bool NARROW>
 __global__ void __launch_bounds__(RS_WARPS * 32) rect_sums_kernel(RectArgs A) {
+  constexpr int NC = NARROW ? 4 : RS_COLS;
   extern __shared__ double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int zsz = A.nrz * A.ncz;
@@ -731,91 +739,95 @@ __global__ void __launch_bounds__(RS_WARPS * 32) rect_sums_kernel(RectArgs A) {
   if (m >= A.n_maps) return;
   const float* img = (view == 0 ? A.maps[0] : A.maps[1]) + m * (int64_t)A.p * A.q;
   for (int e = lane; e < zsz; e += 32) Zp[e] = 0.0;
-  const bool vec = (A.q & 3) == 0;
+  const bool vec = NARROW || (A.q & 3) == 0;
   // lane columns: vec -> 4*lane + 128*g + k ; scalar -> lane + 32*k
-  int col[RS_COLS];
-  int czc[RS_COLS];
+  int czc[NC];
 #pragma unroll
-  for (int k = 0; k < RS_COLS; ++k) {
-    col[k] = vec ? (4 * lane + 128 * (k >> 2) + (k & 3)) : (lane + 32 * k);
-    czc[k] = col[k] < A.q ? A.cz_of_x[col[k] + A.left] : -1;
+  for (int k = 0; k < NC; ++k) {
+    const int col = vec ? (4 * lane + 128 * (k >> 2) + (k & 3)) : (lane + 32 * k);
+    czc[k] = col < A.q ? A.cz_of_x[col + A.left] : -1;
   }
   __syncwarp();
   const int big = A.big_cz;
-  int y = 0;
-  for (int rz = 0; rz < A.nrz; ++rz) {
-    double acc[RS_COLS];
+  double acc[NC];
+  auto flush = [&](int rz) {
+    double s_int = 0.0;
 #pragma unroll
-    for (int k = 0; k < RS_COLS; ++k) acc[k] = 0.0;
-    int ye = y;
-    while (ye < A.Hp && A.rz_of_y[ye] == rz) ++ye;
-    const int i0 = max(y - A.top, 0), i1 = min(ye - A.top, A.p);
-    if (vec && A.q <= 128) {
-      // one float4 per lane per row; 8 rows' loads issued before their sums (HBM latency)
-      const bool live = 4 * lane < A.q;
-      const float* base = img + 4 * lane;
-      int i = i0;
-      for (; i + 8 <= i1; i += 8) {
-        float4 v[8];
+    for (int k = 0; k < NC; ++k) {
+      if (czc[k] >= 0) {
+        if (czc[k] == big) s_int += acc[k];
+        else Zp[rz * A.ncz + czc[k]] = acc[k];  // singleton column zone: this lane's column only
+      }
+      acc[k] = 0.0;
+    }
+    s_int = warp_sum(s_int);
+    if (lane == 0 && big >= 0) Zp[rz * A.ncz + big] = s_int;
+  };
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          v[u] = live ? __ldg(reinterpret_cast<const float4*>(base + (int64_t)(i + u) * A.q)) : make_float4(0, 0, 0, 0);
+  for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+  if constexpr (NARROW) {
+    // one float4 per lane per row; RS_ROWS rows' loads in flight before their sums (HBM latency)
+    const bool live = 4 * lane < A.q;
+    const float* base = img + 4 * lane;
+    int rz = 0;
+    while (A.rz_y0[rz + 1] <= A.top) ++rz;  // zone of image row 0
+    int ynext = A.rz_y0[rz + 1] - A.top;     // first image row of the next zone
+    for (int i = 0; i < A.p; i += RS_ROWS) {
+      float4 v[RS_ROWS];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < RS_ROWS; ++u)
+        v[u] = (live && i + u < A.p) ? __ldg(reinterpret_cast<const float4*>(base + (int64_t)(i + u) * A.q))
+                                      : make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < RS_ROWS; ++u) {
+        if (i + u < A.p) {
+          if (i + u >= ynext) {  // warp-uniform: close the zone, move to the one holding row i + u
+            flush(rz);
+            do { ++rz; } while (A.rz_y0[rz + 1] - A.top <= i + u);
+            ynext = A.rz_y0[rz + 1] - A.top;
+          }
           acc[0] += (double)v[u].x;
           acc[1] += (double)v[u].y;
           acc[2] += (double)v[u].z;
           acc[3] += (double)v[u].w;
         }
       }
-      for (; i < i1; ++i) {
-        const float4 v = live ? __ldg(reinterpret_cast<const float4*>(base + (int64_t)i * A.q)) : make_float4(0, 0, 0, 0);
-        acc[0] += (double)v.x;
-        acc[1] += (double)v.y;
-        acc[2] += (double)v.z;
-        acc[3] += (double)v.w;
-      }
-    } else
-    for (int i = i0; i < i1; ++i) {
-      const float* row = img + (int64_t)i * A.q;
-      if (vec) {
+    }
+    flush(rz);
+  } else {
+    for (int rz = 0; rz < A.nrz; ++rz) {
+      const int i0 = max(A.rz_y0[rz] - A.top, 0), i1 = min(A.rz_y0[rz + 1] - A.top, A.p);
+      if (i0 >= i1) continue;
+      for (int i = i0; i < i1; ++i) {
+        const float* row = img + (int64_t)i * A.q;
+        if (vec) {
 #pragma unroll
-        for (int g = 0; g < RS_COLS / 4; ++g) {
-          const int c0 = 4 * lane + 128 * g;
-          if (c0 < A.q) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(row + c0));
-            acc[4 * g + 0] += (double)v.x;
-            acc[4 * g + 1] += (double)v.y;
-            acc[4 * g + 2] += (double)v.z;
-            acc[4 * g + 3] += (double)v.w;
+          for (int g = 0; g < RS_COLS / 4; ++g) {
+            const int c0 = 4 * lane + 128 * g;
+            if (c0 < A.q) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(row + c0));
+              acc[4 * g + 0] += (double)v.x;
+              acc[4 * g + 1] += (double)v.y;
+              acc[4 * g + 2] += (double)v.z;
+              acc[4 * g + 3] += (double)v.w;
+            }
           }
+        } else {
+#pragma unroll
+          for (int k = 0; k < RS_COLS; ++k)
+            if (lane + 32 * k < A.q) acc[k] += (double)__ldg(row + lane + 32 * k);
         }
-      } else {
-#pragma unroll
-        for (int k = 0; k < RS_COLS; ++k)
-          if (col[k] < A.q) acc[k] += (double)__ldg(row + col[k]);
       }
+      flush(rz);
     }
-    double s_int = 0.0;
-#pragma unroll
-    for (int k = 0; k < RS_COLS; ++k) {
-      if (czc[k] < 0) continue;
-      if (czc[k] == big) s_int += acc[k];
-      else Zp[rz * A.ncz + czc[k]] = acc[k];  // singleton column zone: this lane's column only
-    }
-    s_int = warp_sum(s_int);
-    if (lane == 0 && big >= 0) Zp[rz * A.ncz + big] = s_int;
-    y = ye;
   }
   __syncwarp();
   for (int k = lane; k < A.d; k += 32) {
     const int a = k / A.l2, b = k % A.l2;
+    const int r0 = A.a_rz[2 * a], r1 = A.a_rz[2 * a + 1], c0 = A.b_cz[2 * b], c1 = A.b_cz[2 * b + 1];
     double s = 0.0;
-    for (int rz = 0; rz < A.nrz; ++rz) {
-      if (a < A.rz_lo[rz] || a > A.rz_hi[rz]) continue;
-      for (int cz = 0; cz < A.ncz; ++cz)
-        if (b >= A.cz_lo[cz] && b <= A.cz_hi[cz]) s += Zp[rz * A.ncz + cz];
-    }
+    for (int rz = r0; rz <= r1; ++rz)
+      for (int cz = c0; cz <= c1; ++cz) s += Zp[rz * A.ncz + cz];
     R[k] = s;
   }
   __syncwarp();
@@ -1095,7 +1107,8 @@ static void lag_layout(const Geo& g, int nb, int64_t max_maps, int64_t n_maps, L
   L->off_Z = take(sizeof(double) * (size_t)nb * 2 * L->P.nrz * L->P.ncz * L->P.NDF);
   L->off_zoff = take(sizeof(int) * (L->P.nrz * L->P.ncz + 1));
   L->off_zlist = take(sizeof(int) * L->P.nrec);
-  L->off_zones = take(sizeof(int) * (2 * L->P.nrz + 2 * L->P.ncz + g.Hp + g.Wp));
+  // zone tables + rect_sums helpers: row start of each row zone, covering zone range per tap row / column
+  L->off_zones = take(sizeof(int) * (2 * L->P.nrz + 2 * L->P.ncz + g.Hp + g.Wp + (L->P.nrz + 1) + 2 * g.l1 + 2 * g.l2));
   L->off_msum = take(sizeof(double) * 2 * (size_t)n_maps * g.d);
   L->off_ids = take(sizeof(int) * L->P.tasks.size());
   L->total = o;
@@ -1187,6 +1200,22 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
     zones.insert(zones.end(), P.z.cz_hi.begin(), P.z.cz_hi.end());
     zones.insert(zones.end(), P.z.rz_of_y.begin(), P.z.rz_of_y.end());
     zones.insert(zones.end(), P.z.cz_of_x.begin(), P.z.cz_of_x.end());
+    // rect_sums: first padded row of each row zone (+ Hp), and for each tap row a / column b the
+    // contiguous range of zones covering it (zones are intervals sorted by position)
+    for (int rz = 0, y = 0; rz < P.nrz; ++rz) {
+      while (P.z.rz_of_y[y] != rz) ++y;
+      zones.push_back(y);
+    }
+    zones.push_back(g.Hp);
+    auto cover = [&](const std::vector<int>& lo, const std::vector<int>& hi, int v) {
+      int f = -1, l = -2;
+      for (int z = 0; z < (int)lo.size(); ++z)
+        if (v >= lo[z] && v <= hi[z]) { if (f < 0) f = z; l = z; }
+      zones.push_back(f);
+      zones.push_back(l);
+    };
+    for (int a = 0; a < g.l1; ++a) cover(P.z.rz_lo, P.z.rz_hi, a);
+    for (int b = 0; b < g.l2; ++b) cover(P.z.cz_lo, P.z.cz_hi, b);
     {
       const Upload parts[] = {
           {td.data(), sizeof(TaskDev) * td.size(), w + L.off_tasks},
@@ -1203,6 +1232,9 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
     const int *rz_lo = zd, *rz_hi = zd + P.nrz, *cz_lo = zd + 2 * P.nrz, *cz_hi = zd + 2 * P.nrz + P.ncz;
     const int* rz_of_y = zd + 2 * P.nrz + 2 * P.ncz;
     const int* cz_of_x = rz_of_y + g.Hp;
+    const int* rz_y0 = cz_of_x + g.Wp;
+    const int* a_rz = rz_y0 + P.nrz + 1;
+    const int* b_cz = a_rz + 2 * g.l1;
 
     LagArgs A;
     A.maps[0] = maps1;
@@ -1325,14 +1357,20 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
       RectArgs R;
       R.maps[0] = maps1; R.maps[1] = maps2;
       R.out = reinterpret_cast<double*>(w + L.off_msum);
-      R.rz_of_y = rz_of_y; R.cz_of_x = cz_of_x; R.rz_lo = rz_lo; R.rz_hi = rz_hi; R.cz_lo = cz_lo; R.cz_hi = cz_hi;
+      R.rz_y0 = rz_y0; R.cz_of_x = cz_of_x; R.a_rz = a_rz; R.b_cz = b_cz;
       R.n_maps = n_maps; R.p = g.p; R.q = g.q; R.top = g.top; R.left = g.left; R.Hp = g.Hp; R.Wp = g.Wp;
       R.nrz = P.nrz; R.ncz = P.ncz; R.l1 = g.l1; R.l2 = g.l2; R.d = g.d; R.center = center;
       R.big_cz = P.z.big_cz;
       if (g.q > 32 * RS_COLS) return fail(DDCCA_ECONFIG, "moments: maps wider than %d columns", 32 * RS_COLS);
       const size_t sm = sizeof(double) * RS_WARPS * ((size_t)P.nrz * P.ncz + g.d);
-      cudaFuncSetAttribute(rect_sums_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      rect_sums_kernel<<<dim3((unsigned)((n_maps + RS_WARPS - 1) / RS_WARPS), 2), RS_WARPS * 32, sm, st>>>(R);
+      const dim3 rgrid((unsigned)((n_maps + RS_WARPS - 1) / RS_WARPS), 2);
+      if (g.q % 4 == 0 && g.q <= 128) {
+        cudaFuncSetAttribute(rect_sums_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        rect_sums_kernel<true><<<rgrid, RS_WARPS * 32, sm, st>>>(R);
+      } else {
+        cudaFuncSetAttribute(rect_sums_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        rect_sums_kernel<false><<<rgrid, RS_WARPS * 32, sm, st>>>(R);
+      }
       DDCCA_TRY(check_launch("moments: rect_sums"));
       batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(R.out, map_label, A.batch_off, n_maps, g.d,
                                                                  class_count, plen, cols_per_map, partials);
