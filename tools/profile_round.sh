@@ -2,7 +2,8 @@
 # Profile evidence for one round (run under gpurun from the repo root, ONE GPU):
 #   1) the bench command plain (must exit 0 before any ncu pass),
 #   2) its per-launch list (gpu__time_duration + DRAM bytes, --clock-control none),
-#   3) one full capture of each dominant kernel (fused conv-hist, lag moments, conv).
+#   3) one full capture of each dominant kernel (fused conv-hist, lag moments, conv) and of the
+#      HBM-bound window sums (rect_sums).
 # Usage: tools/profile_round.sh [workload]   -> gpurun_out/prof_round/
 set -u
 WL=${1:-caltech256}
@@ -19,4 +20,6 @@ ncu --set full --import-source on --clock-control none -k regex:"lag_tma_kernel"
     -o $OUT/lag_tma $CMD > $OUT/ncu_full2.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"conv_c_kernel" -s 2 -c 1 \
     -o $OUT/conv_c $CMD > $OUT/ncu_full3.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:"rect_sums_kernel" -s 1 -c 1 \
+    -o $OUT/rect_sums $CMD > $OUT/ncu_full4.log 2>&1
 echo "profile rc=$?"
