@@ -179,7 +179,12 @@ DDCCA_API int ddcca_conv_hash(const float* in, int64_t n_maps, const ddcca_geom*
  * block. DDCCA_ECONFIG means "shape not covered" (use ddcca_conv /
  * ddcca_conv_hash + ddcca_block_hist). ddcca_conv_hist_hw fuses the last
  * layer's conv, sign hash and non-overlapping block histograms (K6-final +
- * K7 + K8): counts are written as in ddcca_block_hist, n_bits = count. */
+ * K7 + K8): counts are written as in ddcca_block_hist, n_bits = count.
+ * `center` of ddcca_conv_hist_hw: bit 0 = the layer centers its patches
+ * (LayerConfig.center); DDCCA_CONV_RESPONSES = the inputs are filter
+ * responses of a previous layer (zero-mean), so the float32 shift that keeps
+ * image DC out of the sums is skipped (same results within float32 rounding). */
+#define DDCCA_CONV_RESPONSES 2
 DDCCA_API int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack_host,
                             int count, int center, float* out, void* stream);
 DDCCA_API int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack_host,

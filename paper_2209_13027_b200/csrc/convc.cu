@@ -42,6 +42,7 @@ struct CArgs {
   const float* in;
   int64_t n_maps;
   int p, q, top, left, oh, ow, count, center;
+  int responses;  // conv_hist: input maps are filter responses (DDCCA_CONV_RESPONSES)
   void* out;
   // fused histogram
   int bh, bw, nby, nbx, br, kind, nbits;
@@ -68,10 +69,10 @@ __host__ __device__ inline int cc_buf_elems(int rows_in, int wt) { return (rows_
 // Each staged input row feeds the PY output rows it overlaps, so one row of x values
 // and one row of taps serve PY * PX * NF FFMAs.
 // Tile column v + SH holds padded column v.
-template <int L1, int L2, int NF, int PX, int PY, int SH, bool F2 = false>
+template <int L1, int L2, int NF, int PX, int PY, int SH, bool F2 = false, bool CEN = true>
 __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const float* __restrict__ tile, int Wt, int r0,
                                          int v0, bool center, float (&acc)[PY][PX][NF]) {
-  const float c = center ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + SH + (L2 - 1) / 2] : 0.f;
+  const float c = (CEN && center) ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + SH + (L2 - 1) / 2] : 0.f;
 #pragma unroll
   for (int y = 0; y < PY; ++y)
 #pragma unroll
@@ -93,7 +94,7 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
     }
     float x[NX];
 #pragma unroll
-    for (int t = 0; t < NX; ++t) x[t] = xr[t + SH] - c;
+    for (int t = 0; t < NX; ++t) x[t] = CEN ? xr[t + SH] - c : xr[t + SH];
 #pragma unroll
     for (int y = 0; y < PY; ++y) {
       const int ta = a - y;  // tap row of output row y that reads input row a
@@ -260,7 +261,9 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
 // Fused last layer: sign codes of BR block-rows go straight into per-block shared
 // bins (packed u16 pairs, CTA-wide atomics); then one warp per block writes the
 // counts into the feature row and clears the bins.
-template <int L1, int L2, int NF, int PX, int PY, int SH, int NT>
+// RESP: the input maps are filter responses of a previous layer (zero-mean on average), so
+// the float32 shift by a window pixel that keeps image DC out of the sums is skipped.
+template <int L1, int L2, int NF, int PX, int PY, int SH, int NT, bool RESP>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) float sm[];
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += NT) {
       const int r = s / G * PY, v0 = (s % G) * PX;
       float acc[PY][PX][NF];
-      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_HIST>(T, cur, Wt, r, v0, A.center, acc);
+      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_HIST, !RESP>(T, cur, Wt, r, v0, A.center, acc);
       const int bx0 = v0 / A.bw, rem0 = v0 - bx0 * A.bw;
       if (v0 + PX <= cols && rem0 + PX <= A.bw) {
         // whole strip inside one block: no per-pixel bounds or block stepping
@@ -456,7 +459,8 @@ static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
                       sizeof(unsigned) * (size_t)A.br * A.nbx * (size_t)((nbins + 1) / 2);
   if (smem > 220 * 1024) return fail(DDCCA_ECONFIG, "conv_hist: band does not fit shared memory");
   const int64_t tiles = A.n_maps * ((A.nby + A.br - 1) / A.br);
-  auto kern = conv_hist_kernel<L1, L2, NF, PX, PY, SH, NT>;
+  auto kern = A.responses ? conv_hist_kernel<L1, L2, NF, PX, PY, SH, NT, true>
+                          : conv_hist_kernel<L1, L2, NF, PX, PY, SH, NT, false>;
   const int grid = persistent_grid(kern, smem, tiles, NT);
   kern<<<grid, NT, smem, st>>>(A, T, tm);
   return check_launch("conv_hist_kernel");
@@ -565,7 +569,7 @@ int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, co
   if (n_maps == 0) return DDCCA_OK;
   CArgs A{};
   A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
-  A.count = count; A.center = center; A.out = nullptr;
+  A.count = count; A.center = center & 1; A.responses = (center & DDCCA_CONV_RESPONSES) ? 1 : 0; A.out = nullptr;
   A.bh = block_h; A.bw = block_w; A.nby = g.oh / block_h; A.nbx = g.ow / block_w; A.kind = count_kind;
   A.nbits = count; A.counts = counts; A.gpr = groups_per_row; A.row_stride = row_stride; A.group_stride = group_stride;
   return dispatch<true>(A, g.l1, g.l2, conv_pack_host, as_stream(stream));

@@ -195,8 +195,11 @@ def conv(ex, maps, layer: DeviceLayer, view: int, out=None):
     return out
 
 
+CONV_RESPONSES = 2  # include/ddcca.h DDCCA_CONV_RESPONSES
+
+
 def conv_hist(ex, maps, layer: DeviceLayer, view: int, plan, counts_base, kind: int, groups_per_row: int,
-              row_stride: int, group_stride: int) -> bool:
+              row_stride: int, group_stride: int, responses: bool = False) -> bool:
     """Fused last-layer conv + sign hash + block histograms; False if the shape is not covered."""
     lib = _native.load()
     hp = layer.host_pack(view)
@@ -205,7 +208,8 @@ def conv_hist(ex, maps, layer: DeviceLayer, view: int, plan, counts_base, kind: 
     n, p, q = maps.shape
     g = layer.geom.native(p, q)
     rc = lib.ddcca_conv_hist_hw(_native.ptr(maps), n, C.byref(g), hp.ctypes.data_as(C.c_void_p), layer.count,
-                                int(layer.center), plan.bh, plan.bw, _native.ptr(counts_base), kind, groups_per_row,
+                                int(layer.center) | (CONV_RESPONSES if responses else 0), plan.bh, plan.bw,
+                                _native.ptr(counts_base), kind, groups_per_row,
                                 row_stride, group_stride, _native.stream_ptr(ex.stream))
     if rc == _native.ECONFIG:
         return False
@@ -582,7 +586,8 @@ class Engine:
                     fl_f = 2.0 * n * plan.nby * plan.bh * nb_cols * last.count * last.geom.dim
                     by_f = 4.0 * n * pp * qq + n * plan.blocks * plan.bins * out.element_size()
                     if self._timed("conv_hist", 1, {"kind": "fma", "flops": fl_f, "bytes": by_f}, conv_hist, ex, maps,
-                                   last, view, plan, base, kind, groups, featlen, plan.blocks * plan.bins):
+                                   last, view, plan, base, kind, groups, featlen, plan.blocks * plan.bins,
+                                   len(layers) > 1):
                         continue
                     codes = self._timed("conv_hash", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv_hash, ex,
                                         maps, last, view)
