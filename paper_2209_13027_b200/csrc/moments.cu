@@ -1225,7 +1225,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
           {zlist.data(), sizeof(int) * zlist.size(), w + L.off_zlist},
           {zones.data(), sizeof(int) * zones.size(), w + L.off_zones},
       };
-      DDCCA_TRY(staged_upload(parts, 6, st));
+      DDCCA_TRY(upload_parts(parts, 6, st));
     }
     DDCCA_TRY(check_launch("moments: plan upload"));
     const int* zd = reinterpret_cast<const int*>(w + L.off_zones);
@@ -1298,7 +1298,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
         ids_all.insert(ids_all.end(), ids_short.begin(), ids_short.end());
         {
           const Upload ids_part{ids_all.data(), sizeof(int) * ids_all.size(), ids_dev};
-          DDCCA_TRY(staged_upload(&ids_part, 1, st));
+          DDCCA_TRY(upload_parts(&ids_part, 1, st));
         }
         auto tgo = [&](auto kern) {
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
@@ -1391,7 +1391,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
   double* msum = reinterpret_cast<double*>(w + o_msum);
   {
     const Upload boff_part{batch_offsets_host, sizeof(int64_t) * (n_batches + 1), boff};
-    DDCCA_TRY(staged_upload(&boff_part, 1, st));
+    DDCCA_TRY(upload_parts(&boff_part, 1, st));
   }
   const size_t sm = sizeof(double) * DIRECT_K * g.d;
   cudaFuncSetAttribute(direct_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
