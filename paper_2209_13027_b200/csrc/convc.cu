@@ -400,6 +400,7 @@ static int persistent_grid(K kern, size_t smem, int64_t tiles, int threads = CC_
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (const char* e = getenv("DDCCA_CONV_CTAS_PER_SM")) per_sm = std::min(per_sm, std::max(1, atoi(e)));  // A/B only
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(1, per_sm) * sms));
   return (int)grid;
 }
