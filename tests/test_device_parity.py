@@ -316,10 +316,16 @@ def test_constant_bank_conv_matches_oracle(ex, l, count, p, q):
 
 @pytest.mark.parametrize("l,count,p,q,bh,bw", [(7, 8, 64, 48, 16, 16), (5, 8, 28, 23, 7, 7), (9, 12, 40, 40, 8, 8),
                                                (3, 4, 17, 19, 4, 5), (7, 8, 33, 65, 16, 16), (5, 6, 20, 20, 20, 20)])
-def test_fused_conv_hist_matches_oracle(ex, l, count, p, q, bh, bw):
+@pytest.mark.parametrize("responses", [True, False])
+def test_fused_conv_hist_matches_oracle(ex, l, count, p, q, bh, bw, responses):
+    # responses: zero-mean inputs through the unshifted kernel (DDCCA_CONV_RESPONSES, a hidden
+    # layer's output); else image-like inputs in [0, 1] through the shifted one
     rng = np.random.default_rng(l + count + bh)
     n_in, b = 3, 4
-    maps = rng.standard_normal((b * n_in, p, q)).astype(np.float32)
+    if responses:
+        maps = rng.standard_normal((b * n_in, p, q)).astype(np.float32)
+    else:
+        maps = rng.uniform(size=(b * n_in, p, q)).astype(np.float32)
     f = rng.standard_normal((count, l, l))
     geom = P.PatchGeometry(l, l)
     enc = P.EncoderConfig(bh, bw)
@@ -330,7 +336,7 @@ def test_fused_conv_hist_matches_oracle(ex, l, count, p, q, bh, bw):
         lay = E.layer_from_filters(ex, f, f, geom, True)
         out = torch.zeros((b, featlen), dtype=torch.int16 if kind == 2 else torch.uint8, device=ex.device)
         ok = E.conv_hist(ex, torch.from_numpy(maps).to(ex.device), lay, 1, plan, out.view(-1), kind, n_in, featlen,
-                         plan.blocks * plan.bins)
+                         plan.blocks * plan.bins, responses)
         assert ok
         got = E.decode_counts(out.cpu().numpy(), plan)
     resp = O.conv_stack(maps, O.Layer(f, f, O.Geometry(l, l), True), 1)  # (b*n_in, count, p, q)
