@@ -841,28 +841,49 @@ __global__ void __launch_bounds__(RS_WARPS * 32) rect_sums_kernel(RectArgs A) {
 // ----------------------------------------------------------------------------
 // batch_epilogue: class sums S (d x C), global sums g, counts
 // ----------------------------------------------------------------------------
+constexpr size_t EPI_SMEM_MAX = 160 * 1024;  // class-sum staging in shared memory up to this size
+
+// Class sums S (d x C, accumulated in shared memory when it fits, else in place), global
+// sums g and counts of one (batch, view). Maps of one sample share a label and are
+// contiguous, so each thread adds a run of equal labels in registers and touches S
+// once per run (the same left-to-right order per element as a per-map update).
 __global__ void batch_epilogue_kernel(const double* __restrict__ msum, const int32_t* __restrict__ label,
                                       const int64_t* __restrict__ batch_off, int64_t n_maps, int d, int C,
                                       int64_t plen, double cols_per_map, double* __restrict__ payload) {
+  extern __shared__ double sS[];
   const int batch = blockIdx.x;
   const int view = blockIdx.y;
   const PayloadView pv = payload_view(d, C);
   double* P = payload + (int64_t)batch * plen;
   double* S = P + (view == 0 ? pv.s1 : pv.s2);
   double* g = P + (view == 0 ? pv.g1 : pv.g2);
+  const bool staged = (size_t)d * C * sizeof(double) <= EPI_SMEM_MAX;
+  double* acc = staged ? sS : S;
   const int64_t m0 = batch_off[batch], m1 = batch_off[batch + 1];
-  for (int e = threadIdx.x; e < d * C; e += blockDim.x) S[e] = 0.0;
+  for (int e = threadIdx.x; e < d * C; e += blockDim.x) acc[e] = 0.0;
   __syncthreads();
   const double* src = msum + (int64_t)view * n_maps * d;
   for (int k = threadIdx.x; k < d; k += blockDim.x) {
     double gs = 0.0;
+    int lab = -1;
+    double run = 0.0;
     for (int64_t m = m0; m < m1; ++m) {
       const double v = src[m * d + k];
-      S[(int64_t)k * C + label[m]] += v;
+      const int l = label[m];
+      if (l != lab) {  // close the previous run, continue this label's running sum
+        if (lab >= 0) acc[(int64_t)k * C + lab] = run;
+        lab = l;
+        run = acc[(int64_t)k * C + l];
+      }
+      run += v;
       gs += v;
     }
+    if (lab >= 0) acc[(int64_t)k * C + lab] = run;
     g[k] = gs;
   }
+  __syncthreads();
+  if (staged)
+    for (int e = threadIdx.x; e < d * C; e += blockDim.x) S[e] = acc[e];
   if (view == 0) {
     double* cnt = P + pv.ncls;
     for (int c = threadIdx.x; c < C; c += blockDim.x) cnt[c] = 0.0;
@@ -1089,6 +1110,14 @@ struct LagLayout {
   size_t off_tasks, off_lane, off_boff, off_rec, off_Z, off_zoff, off_zlist, off_zones, off_msum, off_ids, total;
   int nzone_rec;  // total entries of zrec_list
 };
+
+// dynamic shared memory of batch_epilogue_kernel (0: class sums accumulated in place)
+static size_t epi_smem(int d, int C) {
+  const size_t b = (size_t)d * C * sizeof(double);
+  if (b > EPI_SMEM_MAX) return 0;
+  cudaFuncSetAttribute(batch_epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+  return b;
+}
 
 static int nsplit_for(int64_t max_maps) {
   int64_t s = (max_maps + MAPS_PER_SPLIT - 1) / MAPS_PER_SPLIT;
@@ -1372,7 +1401,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
         rect_sums_kernel<false><<<rgrid, RS_WARPS * 32, sm, st>>>(R);
       }
       DDCCA_TRY(check_launch("moments: rect_sums"));
-      batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(R.out, map_label, A.batch_off, n_maps, g.d,
+      batch_epilogue_kernel<<<dim3(n_batches, 2), 128, epi_smem(g.d, class_count), st>>>(R.out, map_label, A.batch_off, n_maps, g.d,
                                                                  class_count, plen, cols_per_map, partials);
       DDCCA_TRY(check_launch("moments: batch_epilogue"));
     }
@@ -1402,7 +1431,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
   direct_map_sums_kernel<<<dim3((unsigned)n_maps, 2), 128, sizeof(double) * g.d, st>>>(maps1, maps2, n_maps, g, center,
                                                                                       msum);
   DDCCA_TRY(check_launch("moments: direct_map_sums"));
-  batch_epilogue_kernel<<<dim3(n_batches, 2), 128, 0, st>>>(msum, map_label, boff, n_maps, g.d, class_count, plen,
+  batch_epilogue_kernel<<<dim3(n_batches, 2), 128, epi_smem(g.d, class_count), st>>>(msum, map_label, boff, n_maps, g.d, class_count, plen,
                                                              cols_per_map, partials);
   return check_launch("moments: batch_epilogue");
 }
