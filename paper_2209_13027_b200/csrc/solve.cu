@@ -189,15 +189,19 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
           const double apq = a[p * n + q];
           if (apq != 0.0) {
             // theta = (a_qq - a_pp) / (2 a_pq), t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)),
-            // c = 1 / sqrt(t^2 + 1), s = t c (solver.py:32-46), with numerator and denominator
-            // of t scaled by |2 a_pq|: one division, one sqrt and one rsqrt on the round's
-            // critical path instead of three divisions and two square roots.
+            // c = 1 / sqrt(t^2 + 1), s = t c (solver.py:32-46), i.e. the rotation by the smaller
+            // angle phi with cos 2phi = |d| / rho, rho = sqrt(d^2 + (2 a_pq)^2). Evaluated as
+            // c = sqrt(h), h = (1 + |d| / rho) / 2, s = sgn(theta) |2 a_pq| / (2 rho c): two
+            // reciprocal square roots on the round's critical path, no division (no cancellation:
+            // h is in [1/2, 1]).
             const double dlt = a[q * n + q] - a[p * n + p];
             const double two = 2.0 * apq;
             const double sg = ((dlt >= 0.0) == (two > 0.0)) || dlt == 0.0 ? 1.0 : -1.0;
-            const double tt = sg * fabs(two) / (fabs(dlt) + sqrt(fma(dlt, dlt, two * two)));
-            c = rsqrt(fma(tt, tt, 1.0));
-            sn = tt * c;
+            const double ri = rsqrt(fma(dlt, dlt, two * two));  // 1 / rho
+            const double h = fma(0.5 * fabs(dlt), ri, 0.5);
+            const double ci = rsqrt(h);                          // 1 / c
+            c = h * ci;
+            sn = sg * (0.5 * fabs(two)) * ri * ci;
           } else {
             q = -1;
           }
