@@ -98,6 +98,11 @@ DDCCA_API int ddcca_moments_partial(const float* maps1, const float* maps2, cons
  * exact). Meant for layers whose inputs are filter responses (no DC term);
  * applies to the TMA lag path (q % 4 == 0, 5x5 / 7x7 / 9x9), exact elsewhere. */
 #define DDCCA_MOMENTS_F32_BLOCKS 1
+/* DDCCA_MOMENTS_FINE_SPLITS: batches of <= 128 maps (one map per sample) are
+ * split into 32-map slices instead of one 128-map slice (4x the CTAs of a
+ * first layer). Split boundaries never depend on the other batches of the
+ * call, so each batch's partial is the same in any call or on any rank. */
+#define DDCCA_MOMENTS_FINE_SPLITS 2
 DDCCA_API int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32_t* map_label,
                              const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* g,
                              int center, int class_count, double* partials, void* ws, size_t ws_bytes,

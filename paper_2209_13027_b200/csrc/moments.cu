@@ -173,6 +173,7 @@ struct LagArgs {
   const int64_t* batch_off; // device copy of batch map offsets
   double* rec;              // [batch][view][split][nrec][NDF]
   int p, q, top, left, Wp, l2, G, NDX, NDF, nrec, nsplit, nbatch, xend;
+  int64_t per_split;        // maps per split: split s of a batch owns its maps [s*per, (s+1)*per)
 };
 
 // Sum over rows [0, nrows) of one staged map tile (float64, row stride tc) of
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1)) lag_zone_kernel(LagArg
   const int xs = T.x0 - (A.l2 - 1);
   const int64_t m_begin = A.batch_off[batch];
   const int64_t m_end = A.batch_off[batch + 1];
-  const int64_t per = (m_end - m_begin + A.nsplit - 1) / A.nsplit;
+  const int64_t per = A.per_split;
   const int64_t ma = m_begin + (int64_t)split * per;
   const int64_t mbnd = min(m_end, ma + per);
   const float* src = view == 0 ? A.maps[0] : A.maps[1];
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
   uint64_t* empty = full + NS;
   const int64_t m_begin = A.batch_off[batch];
   const int64_t m_end = A.batch_off[batch + 1];
-  const int64_t per = (m_end - m_begin + A.nsplit - 1) / A.nsplit;
+  const int64_t per = A.per_split;
   const int64_t ma = m_begin + (int64_t)split * per;
   const int64_t mbnd = min(m_end, ma + per);
   const int nstages = ma < mbnd ? (int)((mbnd - ma + mb - 1) / mb) : 0;
@@ -902,7 +903,8 @@ constexpr int DIRECT_K = 64;  // patches staged per step
 constexpr int DIRECT_ENT = 8; // Gram entries per thread per pass
 
 __global__ void direct_gram_kernel(const float* maps1, const float* maps2, const int64_t* batch_off, Geo g,
-                                   int center, int nsplit, double* rec /* [batch][view][split][d*d] */) {
+                                   int center, int nsplit, int64_t per_cols,
+                                   double* rec /* [batch][view][split][d*d] */) {
   extern __shared__ double stage[];  // [DIRECT_K][d]
   const int split = blockIdx.x;
   const int batch = blockIdx.y;
@@ -912,7 +914,7 @@ __global__ void direct_gram_kernel(const float* maps1, const float* maps2, const
   const int64_t m0 = batch_off[batch], m1 = batch_off[batch + 1];
   const int64_t cols_per_map = (int64_t)g.oh * g.ow;
   const int64_t ncols = (m1 - m0) * cols_per_map;
-  const int64_t per = (ncols + nsplit - 1) / nsplit;
+  const int64_t per = per_cols;  // fixed columns per split (independent of the other batches)
   const int64_t c0 = (int64_t)split * per, c1 = min(ncols, c0 + per);
   const int nent = d * d;
   double* out = rec + (((int64_t)batch * 2 + view) * nsplit + split) * nent;
@@ -1119,14 +1121,27 @@ static size_t epi_smem(int d, int C) {
   return b;
 }
 
-static int nsplit_for(int64_t max_maps) {
-  int64_t s = (max_maps + MAPS_PER_SPLIT - 1) / MAPS_PER_SPLIT;
-  return (int)std::max<int64_t>(1, s);
+// Maps per split. A batch's split boundaries depend only on the split size, never on the
+// other batches of the call, so every batch's partial (and the deterministic multi-GPU
+// reduction) is the same whichever call or rank computes it. Fine splits (32 maps) for
+// layers with one map per sample (DDCCA_MOMENTS_FINE_SPLITS, batches of <= 128 maps)
+// give the first layer 4x more CTAs.
+static int64_t split_maps(int64_t max_maps, int flags) {
+  return ((flags & DDCCA_MOMENTS_FINE_SPLITS) && max_maps <= MAPS_PER_SPLIT) ? MAPS_PER_SPLIT / 4 : MAPS_PER_SPLIT;
 }
 
-static void lag_layout(const Geo& g, int nb, int64_t max_maps, int64_t n_maps, LagLayout* L) {
+static int nsplit_for(int64_t max_maps, int64_t per) {
+  return (int)std::max<int64_t>(1, (max_maps + per - 1) / per);
+}
+
+// splits the workspace is sized for (the finer of the two split sizes)
+static int nsplit_ws(int64_t max_maps) {
+  return nsplit_for(max_maps, split_maps(max_maps, DDCCA_MOMENTS_FINE_SPLITS));
+}
+
+static void lag_layout(const Geo& g, int nb, int64_t max_maps, int64_t n_maps, int nsplit, LagLayout* L) {
   make_plan(g, &L->P);
-  L->nsplit = nsplit_for(max_maps);
+  L->nsplit = nsplit;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
   L->off_tasks = take(sizeof(TaskDev) * L->P.tasks.size());
@@ -1161,10 +1176,10 @@ size_t ddcca_moments_workspace(const ddcca_geom* gg, int n_batches, int64_t max_
   const int64_t n_maps = (int64_t)n_batches * max_maps_per_batch;
   if (g.stride == 1 && g.l1 <= MAX_LAG_L && g.l2 <= MAX_LAG_L) {
     LagLayout L;
-    lag_layout(g, n_batches, max_maps_per_batch, n_maps, &L);
+    lag_layout(g, n_batches, max_maps_per_batch, n_maps, nsplit_ws(max_maps_per_batch), &L);
     return L.total;
   }
-  const int nsplit = nsplit_for(max_maps_per_batch);
+  const int nsplit = nsplit_ws(max_maps_per_batch);
   return align_up(sizeof(double) * (size_t)n_batches * 2 * nsplit * g.d * g.d, 256) +
          align_up(sizeof(int64_t) * (n_batches + 1), 256) + align_up(sizeof(double) * 2 * (size_t)n_maps * g.d, 256);
 }
@@ -1180,7 +1195,8 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
                              const int64_t* batch_offsets_host, int n_batches, const ddcca_geom* gg, int center,
                              int class_count, double* partials, void* ws, size_t ws_bytes, int flags,
                              void* stream) {
-  if (flags & ~DDCCA_MOMENTS_F32_BLOCKS) return fail(DDCCA_ECONFIG, "unknown moments flags 0x%x", flags);
+  if (flags & ~(DDCCA_MOMENTS_F32_BLOCKS | DDCCA_MOMENTS_FINE_SPLITS))
+    return fail(DDCCA_ECONFIG, "unknown moments flags 0x%x", flags);
   Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (n_batches < 1) return fail(DDCCA_ECONFIG, "no batches to accumulate");
@@ -1201,7 +1217,8 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
 
   if (g.stride == 1 && g.l1 <= MAX_LAG_L && g.l2 <= MAX_LAG_L) {
     LagLayout L;
-    lag_layout(g, n_batches, max_maps, n_maps, &L);
+    const int64_t per = split_maps(max_maps, flags);
+    lag_layout(g, n_batches, max_maps, n_maps, nsplit_for(max_maps, per), &L);
     if (ws_bytes < L.total) return fail(DDCCA_ECONFIG, "moments workspace too small (%zu < %zu)", ws_bytes, L.total);
     const Plan& P = L.P;
     // upload plan tables (small; pageable H2D copies are staged by the driver)
@@ -1273,7 +1290,7 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
     A.batch_off = reinterpret_cast<const int64_t*>(w + L.off_boff);
     A.rec = reinterpret_cast<double*>(w + L.off_rec);
     A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.Wp = g.Wp; A.l2 = g.l2;
-    A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit;
+    A.G = P.G; A.NDX = P.NDX; A.NDF = P.NDF; A.nrec = P.nrec; A.nsplit = L.nsplit; A.per_split = per;
     A.nbatch = n_batches;
     A.xend = g.left + g.q;
     // F32: three float32 stages; else two float64 compute tiles + two float32 cp.async stages
@@ -1409,7 +1426,8 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
   }
 
   // direct float64 path for stride != 1 (or very tall windows)
-  const int nsplit = nsplit_for(max_maps);
+  const int64_t per_maps = split_maps(max_maps, flags);
+  const int nsplit = nsplit_for(max_maps, per_maps);
   size_t o_rec = 0;
   size_t o_boff = align_up(sizeof(double) * (size_t)n_batches * 2 * nsplit * g.d * g.d, 256);
   size_t o_msum = o_boff + align_up(sizeof(int64_t) * (n_batches + 1), 256);
@@ -1424,7 +1442,8 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
   }
   const size_t sm = sizeof(double) * DIRECT_K * g.d;
   cudaFuncSetAttribute(direct_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  direct_gram_kernel<<<dim3(nsplit, n_batches, 2), 256, sm, st>>>(maps1, maps2, boff, g, center, nsplit, rec);
+  direct_gram_kernel<<<dim3(nsplit, n_batches, 2), 256, sm, st>>>(maps1, maps2, boff, g, center, nsplit,
+                                                                    per_maps * g.oh * g.ow, rec);
   DDCCA_TRY(check_launch("moments: direct_gram"));
   direct_reduce_kernel<<<n_batches * 2, 256, 0, st>>>(rec, nsplit, g.d, plen, partials);
   DDCCA_TRY(check_launch("moments: direct_reduce"));

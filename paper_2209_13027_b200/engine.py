@@ -34,6 +34,7 @@ from .patches import PatchGeometry
 MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
 KEEP_MAPS_BYTES = 48 << 30  # fit keeps the last layer's input maps (both views) for the transform if they fit
 MOMENTS_F32_BLOCKS = 1  # ddcca.h DDCCA_MOMENTS_F32_BLOCKS
+MOMENTS_FINE_SPLITS = 2  # ddcca.h DDCCA_MOMENTS_FINE_SPLITS
 HOST_CHUNK_BATCHES = 4  # sample batches per streamed device->host count copy
 
 
@@ -468,7 +469,10 @@ class Engine:
     def moments_flags(self, layers: list) -> int:
         """Float32-blocked lag products for layers fed by filter responses (ExecSettings.moments)."""
         mode = getattr(self.ex.settings, "moments", "exact")
-        return MOMENTS_F32_BLOCKS if (layers and mode == "blocked") else 0
+        flags = MOMENTS_F32_BLOCKS if (layers and mode == "blocked") else 0
+        if not layers:  # one map per sample: 32-map splits (4x the CTAs of the first layer)
+            flags |= MOMENTS_FINE_SPLITS
+        return flags
 
     def reduce_partials(self, parts, n_global_batches: int, local_batches: range):
         """Merged accumulator over all ranks' batches (fixed tree or sum-allreduce)."""
