@@ -352,7 +352,10 @@ __device__ int inv_sqrt_dev(const double* c, int n, double* r, double* w, double
 // finalize (moments.py:168-193): Cw = S1 S2^T, Cb = g1 g2^T - Cw, Ct = Cw - Cb,
 // C11 = sym(C11) + eps * tr/d * I (same for C22). Returns false on an empty
 // accumulator (NumericalError in the reference).
-__device__ bool finalize_dev(const double* P, int n, int C, double eps, double* fin, Blk& B) {
+// Entries e0, e0 + es, ... of the d x d outputs are this thread's (one CTA: threadIdx.x /
+// blockDim.x; the grid form spreads the C-term dot products over several CTAs). Every
+// CTA evaluates the traces the same way, so the ridge terms do not depend on the grid.
+__device__ bool finalize_dev(const double* P, int n, int C, double eps, double* fin, Blk& B, int e0, int es) {
   const PayloadView pv = payload_view(n, C);
   const int nn = n * n;
   double* c11 = fin;
@@ -361,15 +364,18 @@ __device__ bool finalize_dev(const double* P, int n, int C, double eps, double* 
   double* cb = fin + 3 * nn;
   double* ct = fin + 4 * nn;
   if (!(P[pv.n] >= 1.0)) return false;
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+  for (int e = e0; e < nn; e += es) {
     const int i = e / n, j = e - i * n;
+    const double* r1 = P + pv.s1 + (int64_t)i * C;
+    const double* r2 = P + pv.s2 + (int64_t)j * C;
     double s = 0.0;
-    for (int c = 0; c < C; ++c) s += P[pv.s1 + (int64_t)i * C + c] * P[pv.s2 + (int64_t)j * C + c];
+#pragma unroll 8
+    for (int c = 0; c < C; ++c) s += r1[c] * r2[c];
+    const double b = P[pv.g1 + i] * P[pv.g2 + j] - s;
     cw[e] = s;
-    cb[e] = P[pv.g1 + i] * P[pv.g2 + j] - s;
+    cb[e] = b;
+    ct[e] = s - b;
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) ct[e] = cw[e] - cb[e];
   double tr1 = 0.0, tr2 = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     tr1 += 0.5 * (P[pv.c11 + i * n + i] + P[pv.c11 + i * n + i]);
@@ -378,7 +384,7 @@ __device__ bool finalize_dev(const double* P, int n, int C, double eps, double* 
   tr1 = block_sum(tr1, B);
   tr2 = block_sum(tr2, B);
   const double rid1 = eps * (tr1 / n), rid2 = eps * (tr2 / n);
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+  for (int e = e0; e < nn; e += es) {
     const int i = e / n, j = e - i * n;
     c11[e] = 0.5 * (P[pv.c11 + e] + P[pv.c11 + j * n + i]) + (i == j ? rid1 : 0.0);
     c22[e] = 0.5 * (P[pv.c22 + e] + P[pv.c22 + j * n + i]) + (i == j ? rid2 : 0.0);
@@ -393,9 +399,12 @@ __global__ void __launch_bounds__(SOLVE_THREADS) finalize_kernel(const double* P
   __shared__ int flag;
   __shared__ int iscr[2];
   Blk B{red, &flag, iscr};
-  const bool ok = finalize_dev(P, n, C, eps, fin, B);
-  if (threadIdx.x == 0) *status = ok ? DDCCA_OK : DDCCA_ENUMERICAL;
+  const bool ok = finalize_dev(P, n, C, eps, fin, B, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *status = ok ? DDCCA_OK : DDCCA_ENUMERICAL;
 }
+
+// One output entry per thread: the C-term dot products are latency-bound chains.
+static int finalize_grid(int n) { return (n * n + SOLVE_THREADS - 1) / SOLVE_THREADS; }
 
 struct SolveArgs {
   const double* payload;
@@ -506,7 +515,7 @@ __global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
     if (threadIdx.x == 0) *S.status = 0;
     __syncthreads();
     // ---- finalize (moments.py:168-193); payload == nullptr: fin already holds finalized moments
-    if (S.payload != nullptr && !finalize_dev(S.payload, n, C, S.eps, S.fin, B)) {
+    if (S.payload != nullptr && !finalize_dev(S.payload, n, C, S.eps, S.fin, B, threadIdx.x, blockDim.x)) {
       if (threadIdx.x == 0) *S.status = DDCCA_ENUMERICAL;
       return;
     }
@@ -703,7 +712,7 @@ int ddcca_solve(const double* payload, int dim, int class_count, double epsilon,
   cudaStream_t st = as_stream(stream);
   // finalize -> both whitenings in parallel (two CTAs) -> T, eig(T T^T), filters
   if (payload != nullptr) {
-    finalize_kernel<<<1, SOLVE_THREADS, 0, st>>>(payload, dim, class_count, epsilon, fin, status);
+    finalize_kernel<<<finalize_grid(dim), SOLVE_THREADS, 0, st>>>(payload, dim, class_count, epsilon, fin, status);
   } else {
     cudaMemsetAsync(status, 0, sizeof(int32_t), st);
   }
@@ -718,7 +727,7 @@ int ddcca_finalize(const double* payload, int dim, int class_count, double epsil
                    void* stream) {
   if (dim < 1 || class_count < 1) return fail(DDCCA_ECONFIG, "invalid accumulator shape dim=%d classes=%d", dim, class_count);
   if (epsilon < 0) return fail(DDCCA_ECONFIG, "ridge coefficient %g must be >= 0", epsilon);
-  finalize_kernel<<<1, SOLVE_THREADS, 0, as_stream(stream)>>>(payload, dim, class_count, epsilon, fin, status);
+  finalize_kernel<<<finalize_grid(dim), SOLVE_THREADS, 0, as_stream(stream)>>>(payload, dim, class_count, epsilon, fin, status);
   return check_launch("finalize_kernel");
 }
 
