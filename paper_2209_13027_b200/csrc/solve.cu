@@ -179,10 +179,15 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
     if (offdiag_norm(a, n, B) <= 1e-12) { converged = true; break; }
     PROF_ADD(0, t_off);
     PROF_COUNT_SWEEP();
+    // this thread's pair seats, advanced one seat per round (no integer modulo on the
+    // round's critical path): rr_seat(k, r + 1) = rr_seat(k, r) - 1, wrapping 1 -> m - 1
+    const bool own = (int)threadIdx.x < npair;
+    int su = own ? rr_seat(threadIdx.x, 0, m) : 0, sx = own ? rr_seat(m - 1 - threadIdx.x, 0, m) : 0;
     for (int r = 0; r < m - 1; ++r) {
       PROF_MARK(t_round);
       for (int t = threadIdx.x; t < npair; t += blockDim.x) {
-        const int u = rr_seat(t, r, m), x = rr_seat(m - 1 - t, r, m);
+        const bool mine = t == (int)threadIdx.x;
+        const int u = mine ? su : rr_seat(t, r, m), x = mine ? sx : rr_seat(m - 1 - t, r, m);
         int p = min(u, x), q = max(u, x);
         double c = 1.0, sn = 0.0;
         if (q < n) {
@@ -212,6 +217,10 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
         qq[t] = q;
         cs[2 * t] = c;
         cs[2 * t + 1] = sn;
+      }
+      if (own) {
+        if (su != 0) su = su > 1 ? su - 1 : m - 1;  // seat 0 (k = 0) is fixed
+        sx = sx > 1 ? sx - 1 : m - 1;
       }
       __syncthreads();
       PROF_ADD(1, t_round);
