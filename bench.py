@@ -68,7 +68,7 @@ def peaks():
 # ---------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML, else nvidia-smi -lms 100)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -79,7 +79,40 @@ class ClockSampler:
         self.rows = []
         self.proc = None
 
+    def _nvml_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+        if vis and vis[0].strip().isdigit() and self.idx < len(vis):
+            return int(vis[self.idx])
+        return self.idx
+
+    def _poll_nvml(self, nv, h):
+        """NVML every 2 ms: short timed regions (ORL: ~20 ms) still get samples."""
+        names = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                 ("sw_power_cap", 0x4))
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._halt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = get_reasons(h)
+            except Exception:
+                break
+            self.rows.append(["", str(sm), str(mx), "", ""] + ["Active" if bits & b else "Not Active" for _, b in names])
+            self._halt.wait(0.002)
+
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self._nvml_index())
+            self._halt = threading.Event()
+            self.thread = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.nvml = True
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = False
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -96,13 +129,17 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def stop(self):
-        if self.proc is None:
+        if getattr(self, "nvml", False):
+            self._halt.set()
+            self.thread.join(timeout=5)
+        elif self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         reasons = set()
@@ -113,7 +150,8 @@ class ClockSampler:
                     reasons.add(nm)
         load = [s for s in sm if s > 500] or sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "source": "nvml 2 ms" if getattr(self, "nvml", False) else "nvidia-smi 100 ms"}
 
 
 # ---------------------------------------------------------------------------- CPU reference (oracle)
