@@ -125,7 +125,8 @@ DDCCA_API int ddcca_accumulate_columns(const double* x, const double* y, const i
                              int dim, int class_count, double* payload, void* stream);
 
 /* ---------------------------------------------------------------------
- * K4+K5 — finalize + DCCA solve on device (single CTA, float64 Jacobi)
+ * K4+K5 — finalize + DCCA solve on device (finalize over ceil(d*d/1024) CTAs, then
+ *         float64 Jacobi: two whitening CTAs in parallel, one solve CTA)
  * Replaces: finalize (moments.py:168-193), solve_dcca (solver.py:216-257),
  *           sym_eig / inv_sqrt (solver.py:90-170), reshape_filters
  *           (solver.py:260-272).
