@@ -152,6 +152,39 @@ def test_sym_eig_hard_spectra(ex):
         assert np.abs(w - ref).max() <= 1e-9 * max(np.abs(ref).max(), 1e-300), name
 
 
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8, 17, 24, 25, 48, 49, 64, 65, 81, 100, 130])
+def test_sym_eig_orders(ex, n):
+    """Round-robin seats stepped per round (odd / even orders, one and several parameter
+    warps, shared- and global-memory Jacobi) against numpy's eigenvalues."""
+    rng = np.random.default_rng(100 + n)
+    a = rng.standard_normal((n, n))
+    s = a @ a.T + np.diag(np.linspace(0.0, 1.0, n))
+    w, v = P.sym_eig(s, ex)
+    norm = np.linalg.norm(s)
+    assert np.linalg.norm(s @ v - v * w) <= 1e-9 * norm
+    assert np.abs(v.T @ v - np.eye(n)).max() <= 1e-10
+    ref = np.sort(np.linalg.eigvalsh(s))[::-1]
+    assert np.abs(w - ref).max() <= 1e-10 * np.abs(ref).max()
+    assert np.all(np.diff(w) <= 0)
+
+
+@pytest.mark.parametrize("dim,classes", [(81, 300), (49, 257), (25, 40)])
+def test_finalize_grid_vs_oracle(ex, dim, classes):
+    """finalize over ceil(d^2/1024) CTAs (solve.cu finalize_kernel) vs the oracle's acc_finalize."""
+    rng = np.random.default_rng(dim + classes)
+    cols = 3 * classes
+    x, y = rng.standard_normal((dim, cols)), rng.standard_normal((dim, cols))
+    lab = np.arange(cols) % classes
+    acc_o = O.acc_zeros(dim, classes)
+    O.acc_add_columns(acc_o, x, y, lab)
+    fin_o = O.acc_finalize(acc_o, 1e-4)
+    acc = P.MomentAccumulator.zeros(dim, classes)
+    P.accumulate_batch(acc, x, y, lab, ex)
+    fin = P.finalize(acc, 1e-4, ex)
+    for name in ("c11", "c22", "cw", "cb", "ctilde"):
+        assert rel(getattr(fin, name), getattr(fin_o, name)) <= 1e-12, name
+
+
 def test_sym_eig_errors(ex):
     with pytest.raises(P.ShapeError):
         P.sym_eig(np.array([[1.0, 2.0], [0.0, 1.0]]), ex)
