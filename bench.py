@@ -92,14 +92,16 @@ class ClockSampler:
         get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
         mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self._halt.is_set():
+        while True:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                 bits = get_reasons(h)
             except Exception:
                 break
             self.rows.append(["", str(sm), str(mx), "", ""] + ["Active" if bits & b else "Not Active" for _, b in names])
-            self._halt.wait(0.002)
+            self._first.set()
+            if self._halt.wait(0.002):
+                break
 
     def start(self):
         try:
@@ -107,9 +109,11 @@ class ClockSampler:
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self._nvml_index())
             self._halt = threading.Event()
+            self._first = threading.Event()
             self.thread = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
             self.nvml = True
             self.thread.start()
+            self._first.wait(1.0)  # at least one sample before the timed region starts
             return
         except Exception:
             self.nvml = False
