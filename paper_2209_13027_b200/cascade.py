@@ -202,11 +202,14 @@ def train_layer(inputs: LayerOutput, cfg: LayerConfig, class_count: int, batch: 
     ex = _executor(executor)
     n, m = inputs.n_samples, inputs.n_maps
     p, q = inputs.map_shape
+    lab = np.asarray(inputs.labels)
+    if lab.size and (lab.min() < 0 or lab.max() >= class_count):
+        raise ShapeError(f"label outside [0, {class_count})")  # accumulate_batch, moments.py:91-98
     ranges = batch_partition(n, batch)
     with torch.cuda.stream(ex.stream):
         m1 = _to_dev32(ex, inputs.maps1.reshape(-1, p, q))
         m2 = _to_dev32(ex, inputs.maps2.reshape(-1, p, q))
-        mlab = _labels_dev(ex, np.repeat(np.asarray(inputs.labels), m))
+        mlab = _labels_dev(ex, np.repeat(lab, m))
         offs = np.array([0] + [r.stop * m for r in ranges], dtype=np.int64)
         parts = E.moments_partials(ex, m1, m2, mlab, offs, cfg.geom, cfg.center, class_count)
         merged = E.tree_merge(ex, parts)

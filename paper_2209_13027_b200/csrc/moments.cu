@@ -870,11 +870,14 @@ __global__ void batch_epilogue_kernel(const double* __restrict__ msum, const int
     double run = 0.0;
     for (int64_t m = m0; m < m1; ++m) {
       const double v = src[m * d + k];
-      const int l = label[m];
+      // labels outside [0, C) are a caller error (the Python layer raises ShapeError
+      // first); here they only skip the class sums so the public ABI never writes
+      // out of bounds
+      const int l = ((unsigned)label[m] < (unsigned)C) ? label[m] : -1;
       if (l != lab) {  // close the previous run, continue this label's running sum
         if (lab >= 0) acc[(int64_t)k * C + lab] = run;
         lab = l;
-        run = acc[(int64_t)k * C + l];
+        run = l >= 0 ? acc[(int64_t)k * C + l] : 0.0;
       }
       run += v;
       gs += v;
@@ -890,7 +893,8 @@ __global__ void batch_epilogue_kernel(const double* __restrict__ msum, const int
     for (int c = threadIdx.x; c < C; c += blockDim.x) cnt[c] = 0.0;
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int64_t m = m0; m < m1; ++m) cnt[label[m]] += cols_per_map;
+      for (int64_t m = m0; m < m1; ++m)
+        if ((unsigned)label[m] < (unsigned)C) cnt[label[m]] += cols_per_map;
       P[pv.n] = (double)(m1 - m0) * cols_per_map;
     }
   }
@@ -1053,7 +1057,7 @@ __global__ void columns_partial_kernel(const double* x, const double* y, const i
       double gs = 0.0;
       for (int64_t c = c0; c < c1; ++c) {
         const double v = src[(int64_t)k * cols + c];
-        S[(int64_t)k * C + labels[c]] += v;
+        if ((uint64_t)labels[c] < (uint64_t)C) S[(int64_t)k * C + labels[c]] += v;  // ABI guard
         gs += v;
       }
       o[nent + (int64_t)d * C + k] = gs;
@@ -1078,7 +1082,8 @@ __global__ void columns_reduce_kernel(const double* part, int nblk, const int64_
     }
   }
   if (threadIdx.x == 0) {
-    for (int64_t c = 0; c < cols; ++c) payload[pv.ncls + labels[c]] += 1.0;
+    for (int64_t c = 0; c < cols; ++c)
+      if ((uint64_t)labels[c] < (uint64_t)C) payload[pv.ncls + labels[c]] += 1.0;
     payload[pv.n] += (double)cols;
   }
 }
@@ -1121,13 +1126,14 @@ static size_t epi_smem(int d, int C) {
   return b;
 }
 
-// Maps per split. A batch's split boundaries depend only on the split size, never on the
-// other batches of the call, so every batch's partial (and the deterministic multi-GPU
-// reduction) is the same whichever call or rank computes it. Fine splits (32 maps) for
-// layers with one map per sample (DDCCA_MOMENTS_FINE_SPLITS, batches of <= 128 maps)
+// Maps per split. A batch's split boundaries depend only on the split size (a function of
+// the flags alone, never of the other batches of the call), so every batch's partial (and
+// the deterministic multi-GPU reduction) is the same whichever call or rank computes it.
+// Fine splits (32 maps) for layers with one map per sample (DDCCA_MOMENTS_FINE_SPLITS)
 // give the first layer 4x more CTAs.
 static int64_t split_maps(int64_t max_maps, int flags) {
-  return ((flags & DDCCA_MOMENTS_FINE_SPLITS) && max_maps <= MAPS_PER_SPLIT) ? MAPS_PER_SPLIT / 4 : MAPS_PER_SPLIT;
+  (void)max_maps;
+  return (flags & DDCCA_MOMENTS_FINE_SPLITS) ? MAPS_PER_SPLIT / 4 : MAPS_PER_SPLIT;
 }
 
 static int nsplit_for(int64_t max_maps, int64_t per) {

@@ -199,8 +199,15 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
             // c = sqrt(h), h = (1 + |d| / rho) / 2, s = sgn(theta) |2 a_pq| / (2 rho c): two
             // reciprocal square roots on the round's critical path, no division (no cancellation:
             // h is in [1/2, 1]).
-            const double dlt = a[q * n + q] - a[p * n + p];
-            const double two = 2.0 * apq;
+            double dlt = a[q * n + q] - a[p * n + p];
+            double two = 2.0 * apq;
+            // h and s depend only on the ratio dlt : two; an exact power-of-two rescale keeps
+            // dlt^2 + two^2 from underflowing when both are tiny (the reference's theta form
+            // is scale-invariant). Never taken for entries above 2^-500: bits unchanged there.
+            if (fmax(fabs(dlt), fabs(two)) < 0x1p-500) {
+              dlt *= 0x1p+600;
+              two *= 0x1p+600;
+            }
             const double sg = ((dlt >= 0.0) == (two > 0.0)) || dlt == 0.0 ? 1.0 : -1.0;
             const double ri = rsqrt(fma(dlt, dlt, two * two));  // 1 / rho
             const double h = fma(0.5 * fabs(dlt), ri, 0.5);
@@ -269,7 +276,8 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
   }
   PROF_ADD(3, t_start);
   PROF_MARK(t_post);
-  if (!converged && offdiag_norm(a, n, B) > 1e-12) return DDCCA_ENUMERICAL;
+  // written as !(x <= tol) so a NaN off-diagonal norm is reported, never returned as converged
+  if (!converged && !(offdiag_norm(a, n, B) <= 1e-12)) return DDCCA_ENUMERICAL;
   // eigenvalues, stable descending order
   for (int i = threadIdx.x; i < n; i += blockDim.x) wtmp[i] = a[i * n + i] * norm;
   __syncthreads();

@@ -481,7 +481,6 @@ class Engine:
         levels = max(1, int(math.ceil(math.log2(max(parts.shape[0], 1))))) if parts.shape[0] > 1 else 0
         if ex.world_size == 1:
             return self._timed("tree", levels, None, tree_merge, ex, parts)
-        dist = torch.distributed
         if ex.deterministic:
             # every rank's per-batch partials in global batch order, same tree everywhere:
             # bitwise identical to the single-GPU result for any GPU count
@@ -490,10 +489,10 @@ class Engine:
             with torch.cuda.stream(ex.stream):
                 allp = gather_batch_partials(parts, n_global_batches, ex.world_size, ex.group)
             return tree_merge(ex, allp)
-        merged = tree_merge(ex, parts)
+        from .execution import allreduce_partials
+
         with torch.cuda.stream(ex.stream):
-            dist.all_reduce(merged, group=ex.group)
-        return merged
+            return allreduce_partials(parts, lambda t: tree_merge(ex, t), ex.group)
 
     def fit(self, images1, images2, labels, classes: int, layer_cfgs: list, batch_size: int, eps: float,
             n_global: int | None = None, first_sample: int = 0, keep_stats: bool = False,

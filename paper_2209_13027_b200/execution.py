@@ -132,3 +132,21 @@ def gather_batch_partials(parts, n_global_batches: int, world: int, group=None):
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return torch.cat([b[:c] for b, c in zip(bufs, counts)], dim=0).contiguous()
+
+
+def allreduce_partials(parts, merge, group=None):
+    """Fast-mode reduction: this rank's partials merged locally, then one sum-allreduce.
+
+    ``merge`` maps an (n_local, plen) tensor to its (plen,) merge (the device tree on
+    the GPU path). A rank that owns no batches (more ranks than batches) contributes
+    a zero payload, so every rank still joins the collective and nobody blocks.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if parts.shape[0] == 0:
+        merged = torch.zeros(parts.shape[1], dtype=parts.dtype, device=parts.device)
+    else:
+        merged = merge(parts)
+    dist.all_reduce(merged, group=group)
+    return merged

@@ -100,8 +100,32 @@ def handoff(ex, *tensors) -> None:
             t.record_stream(cur)
 
 
+def feature_rows(ds, config, executor=None) -> range:
+    """Dataset rows whose features this rank's ``compute_features`` returns.
+
+    ``range(0, M)`` without a process group; with one, the rank's contiguous
+    batch shard (the samples train_network accumulated on this rank).
+    """
+    from .patches import batch_partition
+
+    ex = _executor(executor)
+    n = len(ds)
+    gb = batch_partition(n, config.net.batch) if hasattr(config, "net") else [range(0, n)]
+    mine = ex.shard(len(gb))
+    if not len(mine):
+        return range(0, 0)
+    return range(gb[mine.start].start, gb[mine.stop - 1].stop)
+
+
 def compute_features(ds, bank, config, executor=None) -> np.ndarray:
-    """Transform: (M, featlen) float64 IQ features, identical layout to the reference."""
+    """Transform: (M, featlen) float64 IQ features, identical layout to the reference.
+
+    Without a process group this is the reference's full (M, featlen) matrix
+    (pipeline.py:61-86). Under a process group (world > 1) the transform is
+    sharded like the fit: each rank returns only the rows of its batch shard,
+    ``feature_rows(ds, config, executor)``, in dataset order — pair them with
+    ``ds.labels[feature_rows(...)]``, or gather them yourself.
+    """
     import torch
 
     ex = _executor(executor)

@@ -28,3 +28,13 @@ def golden():
         return cache[name]
 
     return load
+
+
+@pytest.fixture(scope="session")
+def golden_json():
+    import json
+
+    def load(name):
+        return json.loads((GOLDEN / f"{name}.json").read_text())
+
+    return load

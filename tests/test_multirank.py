@@ -17,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-from paper_2209_13027_b200.execution import gather_batch_partials, shard_range
+from paper_2209_13027_b200.execution import allreduce_partials, gather_batch_partials, shard_range
 
 
 def _free_port():
@@ -112,3 +112,48 @@ def test_two_rank_reduction_matches_single_process():
     # and the merged payload is the oracle's whole-dataset accumulator
     whole = O.layer_stats(v1[:, None], v2[:, None], lab, O.Geometry(3, 3), True, classes, batch, O.Pool())
     assert np.array_equal(single, _payload(whole))
+
+
+def _empty_rank_worker(rank, world, port, q):
+    """world 3 over 2 batches: rank 2 owns none and must still join both reductions."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        v1, v2, lab, classes, _ = _problem()
+        v1, v2, lab, batch = v1[:8], v2[:8], lab[:8], 4
+        gb = O.batch_ranges(len(lab), batch)
+        mine = shard_range(len(gb), rank, world)
+        if len(mine):
+            local = _batch_payloads(v1, v2, lab, classes, batch, [gb[b] for b in mine])
+        else:
+            plen = 2 * 9 * 9 + 2 * 9 * classes + 2 * 9 + 1 + classes
+            local = np.zeros((0, plen))
+        det = _tree(gather_batch_partials(torch.from_numpy(local), len(gb), world).numpy())
+        fast = allreduce_partials(torch.from_numpy(local), lambda t: torch.from_numpy(_tree(t.numpy())))
+        q.put((rank, len(mine), det, fast.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_without_batches_joins_reductions():
+    """More ranks than batches (engine.reduce_partials): the batchless rank contributes a zero
+    payload in fast mode and padding in deterministic mode; nobody hangs, all agree."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_empty_rank_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    v1, v2, lab, classes, _ = _problem()
+    gb = O.batch_ranges(8, 4)
+    single = _tree(_batch_payloads(v1[:8], v2[:8], lab[:8], classes, 4, gb))
+    assert [n for _, n, _, _ in res] == [1, 1, 0]
+    for _, _, det, fast in res:
+        assert np.array_equal(det, single)
+        assert np.allclose(fast, single, rtol=1e-12, atol=1e-12)
