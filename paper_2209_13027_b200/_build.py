@@ -14,7 +14,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "_lib" / "libddcca.so"
-SOURCES = ["moments.cu", "solve.cu", "conv.cu", "convc.cu", "nn.cu", "views.cu", "io.cu"]
+SOURCES = ["moments.cu", "solve.cu", "conv.cu", "convc.cu", "convtc.cu", "nn.cu", "views.cu", "io.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 COMPILE = [
     "-gencode", "arch=compute_100a,code=sm_100a",

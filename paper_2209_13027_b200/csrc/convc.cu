@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "convtc.cuh"
 #include "tma.cuh"
 
 namespace ddcca {
@@ -573,6 +574,17 @@ int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, co
   A.count = count; A.center = center & 1; A.responses = (center & DDCCA_CONV_RESPONSES) ? 1 : 0; A.out = nullptr;
   A.bh = block_h; A.bw = block_w; A.nby = g.oh / block_h; A.nbx = g.ow / block_w; A.kind = count_kind;
   A.nbits = count; A.counts = counts; A.gpr = groups_per_row; A.row_stride = row_stride; A.group_stride = group_stride;
+  if ((A.responses || !A.center) && g.l1 == g.l2) {
+    // tensor-core kernel (convtc.cu) where no float32 DC shift is needed: filter-response
+    // inputs or uncentered taps; DDCCA_ECONFIG = shape not covered there
+    TcHistArgs t{};
+    t.in = in; t.n_maps = n_maps; t.p = g.p; t.q = g.q; t.top = g.top; t.left = g.left; t.l = g.l1;
+    t.count = count; t.center = A.center; t.bh = A.bh; t.bw = A.bw; t.nby = A.nby; t.nbx = A.nbx;
+    t.kind = count_kind; t.nbits = count; t.counts = counts; t.gpr = groups_per_row; t.row_stride = row_stride;
+    t.group_stride = group_stride;
+    const int rc = conv_hist_tc(t, conv_pack_host, as_stream(stream));
+    if (rc != DDCCA_ECONFIG) return rc;
+  }
   return dispatch<true>(A, g.l1, g.l2, conv_pack_host, as_stream(stream));
 }
 
