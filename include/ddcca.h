@@ -180,9 +180,16 @@ DDCCA_API int ddcca_conv_hash(const float* in, int64_t n_maps, const ddcca_geom*
                     int center, void* codes, void* stream);
 
 /* Constant-bank variants (stride 1, square 3/5/7/9 windows, <= 16 filters):
- * taps come from HOST memory (float32 [d][count], e.g. a host copy of the
- * pack written by ddcca_solve) and are passed to the kernel as a parameter
- * block. DDCCA_ECONFIG means "shape not covered" (use ddcca_conv /
+ * the zero-mean taps of each launch are staged into the library's constant
+ * tap bank on the launching stream, from HOST memory (the _hw entry points:
+ * float32 [d][count], e.g. a host copy of the pack written by ddcca_solve)
+ * or straight from the DEVICE pack ddcca_solve wrote (the _dev entry points:
+ * no host round trip between the solve and the next layer's conv). The bank
+ * is one per device: calls on different streams of one device must be
+ * ordered by the caller. ddcca_conv_hist_* runs on the tcgen05 tensor cores
+ * (3xTF32) when the inputs need no DC shift and the shape is covered (maps of
+ * <= 128 rows, q % 4 == 0, <= 8 filters, 3/5/7 windows; DDCCA_CONV_TC=0
+ * forces the FFMA kernel). DDCCA_ECONFIG means "shape not covered" (use ddcca_conv /
  * ddcca_conv_hash + ddcca_block_hist). ddcca_conv_hist_hw fuses the last
  * layer's conv, sign hash and non-overlapping block histograms (K6-final +
  * K7 + K8): counts are written as in ddcca_block_hist, n_bits = count.
@@ -196,6 +203,11 @@ DDCCA_API int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* g
 DDCCA_API int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack_host,
                                  int count, int center, int block_h, int block_w, void* counts, int count_kind,
                                  int64_t groups_per_row, int64_t row_stride, int64_t group_stride, void* stream);
+DDCCA_API int ddcca_conv_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,
+                             int count, int center, float* out, void* stream);
+DDCCA_API int ddcca_conv_hist_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,
+                                  int count, int center, int block_h, int block_w, void* counts, int count_kind,
+                                  int64_t groups_per_row, int64_t row_stride, int64_t group_stride, void* stream);
 
 /* ---------------------------------------------------------------------
  * K8 — block histograms of code maps (iq_block_features counts,

@@ -54,6 +54,8 @@ _SIGNATURES = {
     "ddcca_sign_hash": (_i32, [_vp, _i64, _i32, _i64, _vp, _vp]),
     "ddcca_conv_hw": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _vp, _vp]),
     "ddcca_conv_hist_hw": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp]),
+    "ddcca_conv_dev": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _vp, _vp]),
+    "ddcca_conv_hist_dev": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp]),
     "ddcca_nn_workspace": (_sz, [_i64, _i64]),
     "ddcca_nn_classify": (_i32, [_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _i32, _vp, _vp, _sz, _vp]),
     "ddcca_counts_to_u16": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp]),

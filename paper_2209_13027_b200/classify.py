@@ -11,10 +11,15 @@ the epilogue, so the distance matrix never exists. Rows are float64 features
 counts ``compute_feature_counts`` leaves in HBM (``CountFeatures``), expanded
 through the IQ LUT inside the kernel's tile staging.
 
-``ridge_one_vs_all``: fitting needs a dense (n x n) or (d x d) eigen-solve of
-the Gram that is not on this path and raises ``ConfigError``; prediction with
-a trained (e.g. loaded) ridge model runs on the device through the same tiled
-GEMM (``ddcca_linear_classify``: largest [x, 1] . w_c, lowest class on ties).
+``ridge_one_vs_all`` (classify.py:86-106): the Gram of the bias-augmented rows
+x = [f, 1] (dual X X' when n <= d + 1, else primal X' X) plus the ridge, its
+eigen-decomposition with the same device Jacobi the filter solve uses
+(``sym_eig``: the reference's round-robin schedule and ordering rules), and
+the one-vs-all targets y = +-1 solved through V diag(1/w) V'; the GEMMs are
+float64 cuBLAS calls on the device (plain library GEMMs, off the hot path).
+The eigen-solve is a single-CTA Jacobi, so the solved dimension (min(n, d + 1))
+is capped at ``RIDGE_MAX_DIM``. Prediction runs through the tiled GEMM
+(``ddcca_linear_classify``: largest [x, 1] . w_c, lowest class on ties).
 """
 
 from __future__ import annotations
@@ -28,6 +33,7 @@ from .errors import ConfigError, ShapeError
 
 CLASSIFIER_KINDS = ("nearest_neighbor", "ridge_one_vs_all")
 NN_METRICS = ("euclidean", "cosine")
+RIDGE_MAX_DIM = 1024  # largest eigen-solve (min(n, d + 1)) the single-CTA Jacobi takes in reasonable time
 
 
 @dataclass
@@ -132,8 +138,8 @@ def fit(features, labels, kind: str = "nearest_neighbor", metric: str = "euclide
     class_count = _check_training_set(n_rows, labels)
     if kind not in CLASSIFIER_KINDS:
         raise ConfigError(f"classifier kind {kind!r} not one of {CLASSIFIER_KINDS}")
-    if kind != "nearest_neighbor":
-        raise ConfigError("ridge_one_vs_all is not on the device path (nearest_neighbor only)")
+    if kind == "ridge_one_vs_all":
+        return _fit_ridge(_executor(executor), features, labels, class_count, lam)
     if metric not in NN_METRICS:
         raise ConfigError(f"metric {metric!r} not one of {NN_METRICS}")
     ex = _executor(executor)
@@ -141,6 +147,46 @@ def fit(features, labels, kind: str = "nearest_neighbor", metric: str = "euclide
     return ClassifierModel(kind=kind, class_count=class_count, metric=metric, train_features=rows,
                            train_labels=labels.copy(), row_kind=row_kind, lut=lut,
                            count_source=features if isinstance(features, CountFeatures) else None)
+
+
+def _fit_ridge(ex, features, labels: np.ndarray, class_count: int, lam) -> ClassifierModel:
+    """One-vs-all ridge regression on [x, 1] (classify.py:86-106), on the device."""
+    import torch
+
+    from . import engine as E
+    from .solver import sym_eig
+
+    with torch.cuda.stream(ex.stream):
+        if isinstance(features, CountFeatures):
+            f = E.Engine(ex).expand(features.counts, features.plan, features.encoder)
+        else:
+            f, _, _ = _rows(ex, features)
+        n, d = f.shape
+        x = torch.cat([f, torch.ones((n, 1), dtype=torch.float64, device=ex.device)], dim=1)
+        if lam is None:
+            lam = 1e-3 * float(torch.sum(x * x).item()) / x.shape[1]
+        if lam <= 0:
+            raise ConfigError(f"ridge lambda {lam} must be > 0")
+        m = min(n, d + 1)
+        if m > RIDGE_MAX_DIM:
+            raise ConfigError(f"ridge fit solves a {m} x {m} eigenproblem; the device Jacobi takes at most "
+                              f"{RIDGE_MAX_DIM} (fewer training rows or features)")
+        lab = torch.from_numpy(labels).to(ex.device)
+        y = torch.where(lab[:, None] == torch.arange(class_count, device=ex.device)[None, :], 1.0, -1.0).to(
+            torch.float64)
+        eye = torch.eye(m, dtype=torch.float64, device=ex.device)
+        g = (x @ x.T if n <= d + 1 else x.T @ x) + lam * eye
+        w_eig, v = sym_eig((0.5 * (g + g.T)).cpu().numpy(), ex)
+        vd = torch.from_numpy(v).to(ex.device)
+        inv = torch.from_numpy(1.0 / w_eig).to(ex.device)
+        if n <= d + 1:
+            # dual form: w = X'(XX' + lam I)^-1 Y
+            solved = (vd * inv) @ (vd.T @ y)
+            weights = (x.T @ solved).T
+        else:
+            weights = ((vd * inv) @ (vd.T @ (x.T @ y))).T
+        out = weights.contiguous().cpu().numpy()
+    return ClassifierModel(kind="ridge_one_vs_all", class_count=class_count, lam=float(lam), weights=out)
 
 
 def predict_many(model: ClassifierModel, features, executor=None) -> np.ndarray:

@@ -34,10 +34,15 @@ constexpr bool CC_FFMA2_CONV = false;
 // still stages them through uniform registers, at more LDCU per FFMA for short strips.)
 constexpr int CC_FULL_UNROLL = 0;
 
-template <int N>
-struct alignas(16) Taps {
-  float w[N];
-};
+// Zero-mean taps of the current launch, [(row * L2 + col) * NF + filter]. Written per
+// launch on the launching stream (cudaMemcpyToSymbolAsync from g_taps_stage, which a
+// one-CTA prep kernel fills from the device filter pack, or from the host pack): the
+// FFMAs read them straight from the constant bank and no host copy of the solve's filters
+// is needed (device-resident hand-off between solve and conv). Launches on one stream are
+// ordered; the entry points document that concurrent streams must be ordered by the caller.
+constexpr int MAX_TAPS = 9 * 9 * 16;
+__constant__ float c_taps[MAX_TAPS];
+__device__ float g_taps_stage[MAX_TAPS];
 
 struct CArgs {
   const float* in;
@@ -71,7 +76,7 @@ __host__ __device__ inline int cc_buf_elems(int rows_in, int wt) { return (rows_
 // and one row of taps serve PY * PX * NF FFMAs.
 // Tile column v + SH holds padded column v.
 template <int L1, int L2, int NF, int PX, int PY, int SH, bool F2 = false, bool CEN = true>
-__device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const float* __restrict__ tile, int Wt, int r0,
+__device__ __forceinline__ void cc_strip(const float* __restrict__ tile, int Wt, int r0,
                                          int v0, bool center, float (&acc)[PY][PX][NF]) {
   const float c = (CEN && center) ? tile[(r0 + (L1 - 1) / 2) * Wt + v0 + SH + (L2 - 1) / 2] : 0.f;
 #pragma unroll
@@ -110,7 +115,7 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
             for (int j = 0; j < PX; ++j)
 #pragma unroll
               for (int g = 0; g < NF; g += 2) {
-                const float2 w2 = make_float2(T.w[(ta * L2 + b) * NF + g], T.w[(ta * L2 + b) * NF + g + 1]);
+                const float2 w2 = make_float2(c_taps[(ta * L2 + b) * NF + g], c_taps[(ta * L2 + b) * NF + g + 1]);
                 const float2 a2 = __ffma2_rn(w2, make_float2(x[j + b], x[j + b]),
                                              make_float2(acc[y][j][g], acc[y][j][g + 1]));
                 acc[y][j][g] = a2.x;
@@ -123,7 +128,7 @@ __device__ __forceinline__ void cc_strip(const Taps<L1 * L2 * NF>& T, const floa
             for (int g = 0; g < NF; ++g)
 #pragma unroll
               for (int j = 0; j < PX; ++j)
-                acc[y][j][g] = fmaf(T.w[(ta * L2 + b) * NF + g], x[j + b], acc[y][j][g]);
+                acc[y][j][g] = fmaf(c_taps[(ta * L2 + b) * NF + g], x[j + b], acc[y][j][g]);
         }
       }
     }
@@ -201,7 +206,7 @@ __device__ __forceinline__ void cc_init_bars(const CArgs& A, uint64_t* bars) {
 // Persistent float-response conv (MODE 0): tiles = (map, band of rows_per_tile output rows).
 template <int L1, int L2, int NF, int PX, int PY, int SH, int NT>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
-    conv_c_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
+    conv_c_kernel(CArgs A, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t bars[2];
   const int G = (A.ow + PX - 1) / PX;
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     if (r < rows_out && u0 + r < A.oh) {
       const int v0 = gi * PX;
       float acc[PY][PX][NF];
-      cc_strip<L1, L2, NF, PX, PY, SH, (CC_FFMA2_CONV || NF > 8)>(T, cur, Wt, r, v0, A.center, acc);
+      cc_strip<L1, L2, NF, PX, PY, SH, (CC_FFMA2_CONV || NF > 8)>(cur, Wt, r, v0, A.center, acc);
 #pragma unroll
       for (int y = 0; y < PY; ++y) {
         const int u = u0 + r + y;
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
 // the float32 shift by a window pixel that keeps image DC out of the sums is skipped.
 template <int L1, int L2, int NF, int PX, int PY, int SH, int NT, bool RESP>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
-    conv_hist_kernel(CArgs A, Taps<L1 * L2 * NF> T, const __grid_constant__ CUtensorMap tmap) {
+    conv_hist_kernel(CArgs A, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t bars[2];
   const int cols = A.nbx * A.bw;                 // only pixels inside blocks are needed
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
     for (int s = threadIdx.x; s < (band_rows + PY - 1) / PY * G; s += NT) {
       const int r = s / G * PY, v0 = (s % G) * PX;
       float acc[PY][PX][NF];
-      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_HIST, !RESP>(T, cur, Wt, r, v0, A.center, acc);
+      cc_strip<L1, L2, NF, PX, PY, SH, CC_FFMA2_HIST, !RESP>(cur, Wt, r, v0, A.center, acc);
       const int bx0 = v0 / A.bw, rem0 = v0 - bx0 * A.bw;
       if (v0 + PX <= cols && rem0 + PX <= A.bw) {
         // whole strip inside one block: no per-pixel bounds or block stepping
@@ -380,6 +385,24 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 3 : 1))
 
 // -------------------------------------------------------------------- host side
 
+// One CTA: zero-mean (per-window centering) taps of a device filter pack, padded to nf filters.
+__global__ void taps_prep_kernel(const float* __restrict__ pack, int count, int d, int nf, int center, float* out) {
+  __shared__ double mean[16];
+  if (threadIdx.x < nf) {
+    double m = 0.0;
+    if (center && (int)threadIdx.x < count) {
+      for (int k = 0; k < d; ++k) m += (double)pack[k * count + threadIdx.x];
+      m /= d;
+    }
+    mean[threadIdx.x] = m;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < d * nf; e += blockDim.x) {
+    const int k = e / nf, g = e - k * nf;
+    out[e] = g < count ? (float)((double)pack[k * count + g] - mean[g]) : 0.f;
+  }
+}
+
 static void zero_mean_taps(const float* pack_host, int count, int d, int nf, bool center, float* out) {
   for (int g = 0; g < nf; ++g) {
     double mean = 0.0;
@@ -390,6 +413,32 @@ static void zero_mean_taps(const float* pack_host, int count, int d, int nf, boo
     for (int k = 0; k < d; ++k)
       out[k * nf + g] = g < count ? (float)((double)pack_host[k * count + g] - mean) : 0.f;
   }
+}
+
+// Zero-mean taps of the launch into g_taps_stage (from the device pack, or the host pack)
+// and, for the FFMA kernels (to_const), on into the constant bank. Stream-ordered.
+static int stage_taps(const float* pack, bool pack_on_device, int count, int d, int nf, bool center, bool to_const,
+                      cudaStream_t st) {
+  if (d * nf > MAX_TAPS) return fail(DDCCA_ECONFIG, "%d taps exceed the constant tap bank", d * nf);
+  if (pack_on_device) {
+    float* stage = nullptr;
+    if (cudaGetSymbolAddress(reinterpret_cast<void**>(&stage), g_taps_stage) != cudaSuccess)
+      return fail(DDCCA_ECUDA, "tap stage symbol");
+    taps_prep_kernel<<<1, 256, 0, st>>>(pack, count, d, nf, center ? 1 : 0, stage);
+    DDCCA_TRY(check_launch("taps_prep_kernel"));
+    if (to_const && cudaMemcpyToSymbolAsync(c_taps, stage, sizeof(float) * d * nf, 0, cudaMemcpyDeviceToDevice, st) !=
+                        cudaSuccess)
+      return fail(DDCCA_ECUDA, "tap bank copy");
+    return DDCCA_OK;
+  }
+  std::vector<float> w((size_t)d * nf);
+  zero_mean_taps(pack, count, d, nf, center, w.data());
+  // pageable host source: staged by the driver before the call returns, so w may go away
+  const cudaError_t e = to_const ? cudaMemcpyToSymbolAsync(c_taps, w.data(), sizeof(float) * d * nf, 0,
+                                                           cudaMemcpyHostToDevice, st)
+                                 : cudaMemcpyToSymbolAsync(g_taps_stage, w.data(), sizeof(float) * d * nf, 0,
+                                                           cudaMemcpyHostToDevice, st);
+  return e == cudaSuccess ? DDCCA_OK : fail(DDCCA_ECUDA, "tap upload: %s", cudaGetErrorString(e));
 }
 
 // Grid for a persistent kernel: resident CTAs per SM x SMs, capped by the tile count.
@@ -421,9 +470,7 @@ static bool cc_tma_map(CArgs& A, int sh, int Wt, int rows_in, CUtensorMap* tm) {
 }
 
 template <int L1, int L2, int NF, int PX, int PY, int SH, int NT = CC_THREADS>
-static int run_conv_c(CArgs A, const float* pack_host, cudaStream_t st) {
-  Taps<L1 * L2 * NF> T;
-  zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
+static int run_conv_c(CArgs A, const float* pack, bool pack_dev, cudaStream_t st) {
   const int G = (A.ow + PX - 1) / PX;
   const int Wt = cc_tile_width(A.ow, L2, PX, SH);
   const int rows_out = PY * std::max(1, NT / G);
@@ -436,14 +483,13 @@ static int run_conv_c(CArgs A, const float* pack_host, cudaStream_t st) {
   const int64_t tiles = A.n_maps * ((A.oh + rows_out - 1) / rows_out);
   auto kern = conv_c_kernel<L1, L2, NF, PX, PY, SH, NT>;
   const int grid = persistent_grid(kern, smem, tiles, NT);
-  kern<<<grid, NT, smem, st>>>(A, T, tm);
+  DDCCA_TRY(stage_taps(pack, pack_dev, A.count, L1 * L2, NF, A.center, true, st));
+  kern<<<grid, NT, smem, st>>>(A, tm);
   return check_launch("conv_c_kernel");
 }
 
 template <int L1, int L2, int NF, int PX, int PY, int SH, int NT = CC_THREADS>
-static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
-  Taps<L1 * L2 * NF> T;
-  zero_mean_taps(pack_host, A.count, L1 * L2, NF, A.center, T.w);
+static int run_conv_hist(CArgs A, const float* pack, bool pack_dev, cudaStream_t st) {
   const int cols = A.nbx * A.bw;
   const int G = (cols + PX - 1) / PX;
   // block rows per CTA: about one strip per thread, two when a block row alone fills at
@@ -464,7 +510,8 @@ static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
   auto kern = A.responses ? conv_hist_kernel<L1, L2, NF, PX, PY, SH, NT, true>
                           : conv_hist_kernel<L1, L2, NF, PX, PY, SH, NT, false>;
   const int grid = persistent_grid(kern, smem, tiles, NT);
-  kern<<<grid, NT, smem, st>>>(A, T, tm);
+  DDCCA_TRY(stage_taps(pack, pack_dev, A.count, L1 * L2, NF, A.center, true, st));
+  kern<<<grid, NT, smem, st>>>(A, tm);
   return check_launch("conv_hist_kernel");
 }
 
@@ -472,27 +519,27 @@ static int run_conv_hist(CArgs A, const float* pack_host, cudaStream_t st) {
 constexpr int same_shift(int l2) { return (4 - ((l2 - 1) / 2) % 4) % 4; }
 
 template <bool HIST, int L, int NF, int PX, int PY, int NT = CC_THREADS>
-static int run_shape(const CArgs& A, const float* pack_host, cudaStream_t st) {
+static int run_shape(const CArgs& A, const float* pack_host, bool pack_dev, cudaStream_t st) {
   constexpr int S = same_shift(L);
   const int want = (4 - A.left % 4) % 4;
   if (S != 0 && want == S) {
-    const int rc = HIST ? run_conv_hist<L, L, NF, PX, PY, S, NT>(A, pack_host, st)
-                        : run_conv_c<L, L, NF, PX, PY, S, NT>(A, pack_host, st);
+    const int rc = HIST ? run_conv_hist<L, L, NF, PX, PY, S, NT>(A, pack_host, pack_dev, st)
+                        : run_conv_c<L, L, NF, PX, PY, S, NT>(A, pack_host, pack_dev, st);
     if (rc != DDCCA_ECONFIG) return rc;
   }
-  return HIST ? run_conv_hist<L, L, NF, PX, PY, 0, NT>(A, pack_host, st)
-              : run_conv_c<L, L, NF, PX, PY, 0, NT>(A, pack_host, st);
+  return HIST ? run_conv_hist<L, L, NF, PX, PY, 0, NT>(A, pack_host, pack_dev, st)
+              : run_conv_c<L, L, NF, PX, PY, 0, NT>(A, pack_host, pack_dev, st);
 }
 
 // Dispatch over the compiled (window, filter-count) shapes; DDCCA_ECONFIG = not covered.
 template <bool HIST>
-static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cudaStream_t st) {
+static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, bool pack_dev, cudaStream_t st) {
   // 8 filters: 16-pixel strips in 128-thread CTAs (3 per SM) halve the tap loads per
   // FFMA; DDCCA_CH8=1 selects the 8-pixel / 256-thread form (A/B)
   const char* ch8 = getenv("DDCCA_CH8");
   if (A.count <= 8 && !(ch8 && ch8[0] == '1')) {
 #define DDCCA_CH(L) \
-    if (l1 == L && l2 == L) return run_shape<HIST, L, 8, 16, 1, 128>(A, pack_host, st);
+    if (l1 == L && l2 == L) return run_shape<HIST, L, 8, 16, 1, 128>(A, pack_host, pack_dev, st);
     DDCCA_CH(3)
     DDCCA_CH(5)
     DDCCA_CH(7)
@@ -503,14 +550,14 @@ static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cuda
   // spends one tap load per 8 FFMAs)
   // wide histograms (2^n_bits > 256 shared bins per block): 8-pixel strips, 256-thread CTAs
   if (HIST && A.nbits > 8 && A.count > 8 && A.count <= 12 && !(ch8 && ch8[0] == '1')) {
-    if (l1 == 7 && l2 == 7) return run_shape<true, 7, 12, 8, 1, 256>(A, pack_host, st);
-    if (l1 == 9 && l2 == 9) return run_shape<true, 9, 12, 8, 1, 256>(A, pack_host, st);
+    if (l1 == 7 && l2 == 7) return run_shape<true, 7, 12, 8, 1, 256>(A, pack_host, pack_dev, st);
+    if (l1 == 9 && l2 == 9) return run_shape<true, 9, 12, 8, 1, 256>(A, pack_host, pack_dev, st);
   }
   // (not for wide histograms: 2^n_bits shared bins per block would leave one small CTA per SM)
   if (A.count > 8 && A.count <= 16 && !(HIST && A.nbits > 8) && !(ch8 && ch8[0] == '1')) {
 #define DDCCA_CH(L, NFV) \
     if (l1 == L && l2 == L && A.count <= NFV && (HIST || NFV <= 12)) \
-      return run_shape<HIST, L, NFV, 8, 1, 128>(A, pack_host, st);
+      return run_shape<HIST, L, NFV, 8, 1, 128>(A, pack_host, pack_dev, st);
     DDCCA_CH(7, 12)
     DDCCA_CH(9, 12)
     DDCCA_CH(3, 16)
@@ -520,7 +567,7 @@ static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cuda
 #undef DDCCA_CH
   }
 #define DDCCA_CC(L, NFV, PXV, PYV) \
-  if (l1 == L && l2 == L && A.count <= NFV) return run_shape<HIST, L, NFV, PXV, PYV>(A, pack_host, st);
+  if (l1 == L && l2 == L && A.count <= NFV) return run_shape<HIST, L, NFV, PXV, PYV>(A, pack_host, pack_dev, st);
   DDCCA_CC(3, 8, 8, 1)
   DDCCA_CC(5, 8, 8, 1)
   DDCCA_CC(7, 8, 8, 1)
@@ -539,25 +586,25 @@ static int dispatch(const CArgs& A, int l1, int l2, const float* pack_host, cuda
 
 using namespace ddcca;
 
-extern "C" {
+namespace {
 
-int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
-                  int center, float* out, void* stream) {
+int conv_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* pack, bool pack_dev, int count,
+               int center, float* out, void* stream) {
   Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (g.stride != 1) return fail(DDCCA_ECONFIG, "constant-bank conv needs stride 1");
   if (count < 1 || count > g.d) return fail(DDCCA_ECONFIG, "filter count %d outside [1, %d]", count, g.d);
-  if (!conv_pack_host) return fail(DDCCA_ESHAPE, "null host taps");
+  if (!pack) return fail(DDCCA_ESHAPE, "null taps");
   if (n_maps == 0) return DDCCA_OK;
   CArgs A{};
   A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
   A.count = count; A.center = center; A.out = out;
-  return dispatch<false>(A, g.l1, g.l2, conv_pack_host, as_stream(stream));
+  return dispatch<false>(A, g.l1, g.l2, pack, pack_dev, as_stream(stream));
 }
 
-int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
-                       int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,
-                       int64_t row_stride, int64_t group_stride, void* stream) {
+int conv_hist_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* pack, bool pack_dev,
+                    int count, int center, int block_h, int block_w, void* counts, int count_kind,
+                    int64_t groups_per_row, int64_t row_stride, int64_t group_stride, void* stream) {
   Geo g{};
   DDCCA_TRY(make_geo(gg, &g));
   if (g.stride != 1) return fail(DDCCA_ECONFIG, "fused conv-histogram needs stride 1");
@@ -567,8 +614,9 @@ int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, co
   const int bpc = block_h * block_w;
   if ((count_kind == 0 && bpc > 255) || (count_kind == 1 && bpc > 510) || bpc > 65535)
     return fail(DDCCA_ECONFIG, "count storage cannot hold %d pixels per block", bpc);
-  if (!conv_pack_host) return fail(DDCCA_ESHAPE, "null host taps");
+  if (!pack) return fail(DDCCA_ESHAPE, "null taps");
   if (n_maps == 0) return DDCCA_OK;
+  cudaStream_t st = as_stream(stream);
   CArgs A{};
   A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
   A.count = count; A.center = center & 1; A.responses = (center & DDCCA_CONV_RESPONSES) ? 1 : 0; A.out = nullptr;
@@ -576,16 +624,50 @@ int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, co
   A.nbits = count; A.counts = counts; A.gpr = groups_per_row; A.row_stride = row_stride; A.group_stride = group_stride;
   if ((A.responses || !A.center) && g.l1 == g.l2) {
     // tensor-core kernel (convtc.cu) where no float32 DC shift is needed: filter-response
-    // inputs or uncentered taps; DDCCA_ECONFIG = shape not covered there
+    // inputs or uncentered taps
     TcHistArgs t{};
     t.in = in; t.n_maps = n_maps; t.p = g.p; t.q = g.q; t.top = g.top; t.left = g.left; t.l = g.l1;
     t.count = count; t.center = A.center; t.bh = A.bh; t.bw = A.bw; t.nby = A.nby; t.nbx = A.nbx;
     t.kind = count_kind; t.nbits = count; t.counts = counts; t.gpr = groups_per_row; t.row_stride = row_stride;
     t.group_stride = group_stride;
-    const int rc = conv_hist_tc(t, conv_pack_host, as_stream(stream));
-    if (rc != DDCCA_ECONFIG) return rc;
+    if (conv_hist_tc_covers(t)) {
+      float* stage = nullptr;
+      if (cudaGetSymbolAddress(reinterpret_cast<void**>(&stage), g_taps_stage) != cudaSuccess)
+        return fail(DDCCA_ECUDA, "tap stage symbol");
+      DDCCA_TRY(stage_taps(pack, pack_dev, count, g.d, TC_FILTERS, A.center, false, st));
+      const int rc = conv_hist_tc(t, stage, st);
+      if (rc != DDCCA_ECONFIG) return rc;
+    }
   }
-  return dispatch<true>(A, g.l1, g.l2, conv_pack_host, as_stream(stream));
+  return dispatch<true>(A, g.l1, g.l2, pack, pack_dev, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
+                  int center, float* out, void* stream) {
+  return conv_entry(in, n_maps, gg, conv_pack_host, false, count, center, out, stream);
+}
+
+int ddcca_conv_dev(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack, int count,
+                   int center, float* out, void* stream) {
+  return conv_entry(in, n_maps, gg, conv_pack, true, count, center, out, stream);
+}
+
+int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack_host, int count,
+                       int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,
+                       int64_t row_stride, int64_t group_stride, void* stream) {
+  return conv_hist_entry(in, n_maps, gg, conv_pack_host, false, count, center, block_h, block_w, counts, count_kind,
+                         groups_per_row, row_stride, group_stride, stream);
+}
+
+int ddcca_conv_hist_dev(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack, int count,
+                        int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,
+                        int64_t row_stride, int64_t group_stride, void* stream) {
+  return conv_hist_entry(in, n_maps, gg, conv_pack, true, count, center, block_h, block_w, counts, count_kind,
+                         groups_per_row, row_stride, group_stride, stream);
 }
 
 }  // extern "C"

@@ -54,10 +54,6 @@ constexpr int RAW_BYTES = 2 * CHUNK_BYTES; // one staged slot: 8 columns
 constexpr int BMAT_BYTES = N * 8 * 4;      // one banded K = 8 chunk, hi or lo
 constexpr int TMEM_COLS = 512;
 
-template <int L>
-struct alignas(16) TapsTc {
-  float w[L * L * NF];  // zero-mean taps, [(dy * L + dx) * NF + f]
-};
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   // K-major, no swizzle: start, leading (K) byte offset, stride (8-row group) byte offset,
@@ -116,7 +112,7 @@ __device__ __forceinline__ void st8(uint32_t taddr, const uint32_t (&v)[8]) {
 
 template <int L>
 __global__ void __launch_bounds__(tc::THREADS, 1)
-    conv_hist_tc_kernel(TcHistArgs A, const __grid_constant__ tc::TapsTc<L> T,
+    conv_hist_tc_kernel(TcHistArgs A, const float* __restrict__ taps /* [(dy * L + dx) * NF + f], zero mean */,
                         const __grid_constant__ CUtensorMap tmap) {
   using namespace tc;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -138,7 +134,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   for (int e = tid; e < L * 4 * N * 8; e += THREADS) {
     const int k = e & 7, n = (e >> 3) % N, hl = (e / (8 * N)) & 1, kc = (e / (16 * N)) & 1, dy = e / (32 * N);
     const int f = n / X, xo = n % X, t = 8 * kc + k - xo - (4 - (L - 1) / 2);
-    const float w = (t >= 0 && t < L) ? T.w[(dy * L + t) * NF + f] : 0.f;
+    const float w = (t >= 0 && t < L) ? taps[(dy * L + t) * NF + f] : 0.f;
     const float hi = tf32_rna(w);
     const float v = hl ? (w - hi) : hi;
     *reinterpret_cast<float*>(bmat + ((dy * 2 + kc) * 2 + hl) * BMAT_BYTES + (k >> 2) * 128 + (n >> 3) * 256 +
@@ -365,19 +361,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 }
 
 template <int L>
-static int launch_tc(const TcHistArgs& a, const float* pack_host, cudaStream_t st) {
+static int launch_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st) {
   using namespace tc;
-  TapsTc<L> T;
-  const int d = L * L;
-  for (int f = 0; f < NF; ++f) {
-    double mean = 0.0;
-    if (a.center && f < a.count) {
-      for (int k = 0; k < d; ++k) mean += (double)pack_host[k * a.count + f];
-      mean /= d;
-    }
-    for (int k = 0; k < d; ++k)
-      T.w[k * NF + f] = f < a.count ? (float)((double)pack_host[k * a.count + f] - mean) : 0.f;
-  }
   const int nbins = 1 << a.nbits;
   size_t smem = (size_t)L * 4 * BMAT_BYTES + (size_t)NS * RAW_BYTES +
                 sizeof(unsigned) * (size_t)a.nby * a.nbx * ((nbins + 1) / 2);
@@ -394,23 +379,27 @@ static int launch_tc(const TcHistArgs& a, const float* pack_host, cudaStream_t s
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(a.n_maps, sms);
-  kern<<<grid, THREADS, smem, st>>>(a, T, tmap);
+  kern<<<grid, THREADS, smem, st>>>(a, taps_dev, tmap);
   return check_launch("conv_hist_tc_kernel");
 }
 
-int conv_hist_tc(const TcHistArgs& a, const float* pack_host, cudaStream_t st) {
+bool conv_hist_tc_covers(const TcHistArgs& a) {
   if (const char* e = getenv("DDCCA_CONV_TC"))
-    if (e[0] == '0') return DDCCA_ECONFIG;  // A/B switch: FFMA kernel
-  // covered: maps of <= 128 rows (one TMEM lane per row), <= 8 filters / 8-bit codes,
-  // odd windows up to 7 (the TMEM A ring of 3 x l x 16 columns plus 2 accumulators)
-  if (a.p > 128 || a.count > tc::NF || a.nbits > 8 || a.n_maps < 1 || a.n_maps > INT32_MAX) return DDCCA_ECONFIG;
-  // TMA staging: 16 B aligned rows and base
-  if (a.q % 4 != 0 || (reinterpret_cast<uintptr_t>(a.in) & 15)) return DDCCA_ECONFIG;
-  if (a.top != (a.l - 1) / 2 || a.left != (a.l - 1) / 2) return DDCCA_ECONFIG;
+    if (e[0] == '0') return false;  // A/B switch: FFMA kernel
+  // maps of <= 128 rows (one TMEM lane per row), <= 8 filters / 8-bit codes, odd windows up
+  // to 7 (the TMEM A ring of 3 x l x 16 columns plus 2 accumulators), TMA-aligned rows
+  if (a.p > 128 || a.count > tc::NF || a.nbits > 8 || a.n_maps < 1 || a.n_maps > INT32_MAX) return false;
+  if (a.q % 4 != 0 || (reinterpret_cast<uintptr_t>(a.in) & 15)) return false;
+  if (a.top != (a.l - 1) / 2 || a.left != (a.l - 1) / 2) return false;
+  return a.l == 3 || a.l == 5 || a.l == 7;
+}
+
+int conv_hist_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st) {
+  if (!conv_hist_tc_covers(a)) return DDCCA_ECONFIG;
   switch (a.l) {
-    case 3: return launch_tc<3>(a, pack_host, st);
-    case 5: return launch_tc<5>(a, pack_host, st);
-    case 7: return launch_tc<7>(a, pack_host, st);
+    case 3: return launch_tc<3>(a, taps_dev, st);
+    case 5: return launch_tc<5>(a, taps_dev, st);
+    case 7: return launch_tc<7>(a, taps_dev, st);
     default: return DDCCA_ECONFIG;
   }
 }

@@ -16,7 +16,12 @@ struct TcHistArgs {
   int64_t gpr, row_stride, group_stride;
 };
 
-// DDCCA_ECONFIG when the shape is not covered (the caller falls back to the FFMA kernel).
-int conv_hist_tc(const TcHistArgs& a, const float* pack_host, cudaStream_t st);
+constexpr int TC_FILTERS = 8;  // filter slots of the tensor-core kernel (zero-padded)
+
+// Shapes the tensor-core kernel takes (else the caller uses the FFMA kernel).
+bool conv_hist_tc_covers(const TcHistArgs& a);
+// taps_dev: zero-mean taps [(dy * l + dx) * TC_FILTERS + f] in device memory (stream-ordered).
+// DDCCA_ECONFIG when the shape is not covered.
+int conv_hist_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st);
 
 }  // namespace ddcca

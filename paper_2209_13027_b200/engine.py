@@ -135,12 +135,12 @@ def solve_layer(ex, payload, geom: PatchGeometry, count: int, center: bool, clas
     layer._status = status
     if check:
         check_layer(layer)
-        fetch_host_packs(layer)
     return layer
 
 
 def fetch_host_packs(layer: DeviceLayer) -> None:
-    """Host copies of the float32 taps (tiny) for the constant-bank conv kernels."""
+    """Host copies of the float32 taps (tiny). The conv kernels read the device packs
+    (ddcca_conv_dev / ddcca_conv_hist_dev); kept for callers of the host-pack entry points."""
     layer.host1 = np.ascontiguousarray(layer.pack1.cpu().numpy())
     layer.host2 = np.ascontiguousarray(layer.pack2.cpu().numpy())
 
@@ -149,6 +149,16 @@ def check_layer(layer: DeviceLayer) -> None:
     st = getattr(layer, "_status", None)
     if st is not None:
         _native.status_error(int(st.item()), "solve_dcca")
+
+
+def check_layers(layers: list) -> None:
+    """Solve statuses of all layers with one device->host read (the end of a fit)."""
+    torch = _torch()
+    sts = [lay._status for lay in layers if getattr(lay, "_status", None) is not None]
+    if not sts:
+        return
+    for code in torch.cat(sts).cpu().tolist():
+        _native.status_error(int(code), "solve_dcca")
 
 
 def layer_from_filters(ex, filters1, filters2, geom: PatchGeometry, center: bool) -> DeviceLayer:
@@ -183,14 +193,13 @@ def conv(ex, maps, layer: DeviceLayer, view: int, out=None):
     if out is None:
         out = torch.empty((n, layer.count, oh, ow), dtype=torch.float32, device=ex.device)
     g = layer.geom.native(p, q)
-    hp = layer.host_pack(view)
-    if hp is not None:
-        rc = lib.ddcca_conv_hw(_native.ptr(maps), n, C.byref(g), hp.ctypes.data_as(C.c_void_p), layer.count,
-                               int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream))
-        if rc == _native.OK:
-            return out
-        if rc != _native.ECONFIG:
-            _native.check(rc, "conv")
+    # constant-bank kernel fed from the device pack (no host copy of the solve's taps)
+    rc = lib.ddcca_conv_dev(_native.ptr(maps), n, C.byref(g), _native.ptr(layer.pack(view)), layer.count,
+                            int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream))
+    if rc == _native.OK:
+        return out
+    if rc != _native.ECONFIG:
+        _native.check(rc, "conv")
     _native.check(lib.ddcca_conv(_native.ptr(maps), n, C.byref(g), _native.ptr(layer.pack(view)), layer.count,
                                  int(layer.center), _native.ptr(out), _native.stream_ptr(ex.stream)), "conv")
     return out
@@ -203,12 +212,11 @@ def conv_hist(ex, maps, layer: DeviceLayer, view: int, plan, counts_base, kind: 
               row_stride: int, group_stride: int, responses: bool = False) -> bool:
     """Fused last-layer conv + sign hash + block histograms; False if the shape is not covered."""
     lib = _native.load()
-    hp = layer.host_pack(view)
-    if hp is None or plan.sh != plan.bh or plan.sw != plan.bw:
+    if plan.sh != plan.bh or plan.sw != plan.bw:
         return False
     n, p, q = maps.shape
     g = layer.geom.native(p, q)
-    rc = lib.ddcca_conv_hist_hw(_native.ptr(maps), n, C.byref(g), hp.ctypes.data_as(C.c_void_p), layer.count,
+    rc = lib.ddcca_conv_hist_dev(_native.ptr(maps), n, C.byref(g), _native.ptr(layer.pack(view)), layer.count,
                                 int(layer.center) | (CONV_RESPONSES if responses else 0), plan.bh, plan.bw,
                                 _native.ptr(counts_base), kind, groups_per_row,
                                 row_stride, group_stride, _native.stream_ptr(ex.stream))
@@ -324,6 +332,14 @@ class Engine:
         self.launches = 0     # kernels launched by this engine
 
     def _timed(self, name: str, kernels: int, work: dict | None, fn, *a, **k):
+        torch = _torch()
+        torch.cuda.nvtx.range_push(name)  # stage ranges for nsys / ncu --nvtx (no-ops otherwise)
+        try:
+            return self._timed_body(name, kernels, work, fn, *a, **k)
+        finally:
+            torch.cuda.nvtx.range_pop()
+
+    def _timed_body(self, name: str, kernels: int, work: dict | None, fn, *a, **k):
         self.launches += kernels
         if work is not None and self.profile is not None:
             acc = self.work.setdefault(name, {"kind": work.get("kind"), "flops": 0.0, "bytes": 0.0, "calls": 0})
@@ -520,11 +536,14 @@ class Engine:
                 parts = self.layer_partials(images1, images2, labels, layers, cfg.geom, cfg.center, classes, local,
                                             first_sample, keep=last and self.keep_maps_bytes > 0)
                 merged = self.reduce_partials(parts, len(gb), mine)
+                # no host round trip between layers: the next layer's convs read this
+                # layer's taps from the device pack, statuses are checked once below
                 layer = self._timed(f"solve_l{i + 1}", 3, None, solve_layer, ex, merged, cfg.geom, cfg.filters,
-                                    cfg.center, classes, eps)
+                                    cfg.center, classes, eps, check=False)
                 layers.append(layer)
                 if keep_stats:
                     stats.append(merged)
+            check_layers(layers)
         self.upload_events = []
         return FitResult(layers, stats)
 

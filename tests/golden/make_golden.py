@@ -295,8 +295,30 @@ def make_models(dd):
                         tied_weights=tied.weights, tied_pred=Cl.predict_many(tied, q))
 
 
+def make_ridge_fit(dd):
+    """Reference ridge fits (classify.py:86-106): primal (n > d + 1) and dual (n <= d + 1) forms,
+    default and explicit lambda, with the reference's predictions on held-out queries."""
+    from ddccanet import classify as Cl
+
+    rng = np.random.default_rng(17)
+    rec = {}
+    for k, (n, d, classes, lam) in enumerate([(60, 12, 4, None), (40, 90, 5, None), (30, 30, 3, 0.5)]):
+        centers = rng.standard_normal((classes, d)) * 2.0
+        labels = np.arange(n) % classes
+        x = centers[labels] + rng.standard_normal((n, d))
+        q = centers[np.arange(25) % classes] + rng.standard_normal((25, d))
+        m = Cl.fit(x, labels, kind="ridge_one_vs_all", lam=lam)
+        rec[f"x{k}"], rec[f"labels{k}"], rec[f"q{k}"] = x, labels, q
+        rec[f"lam_in{k}"] = np.array(-1.0 if lam is None else lam)
+        rec[f"lam{k}"], rec[f"weights{k}"] = np.array(m.lam), m.weights
+        rec[f"pred{k}"] = Cl.predict_many(m, q)
+    np.savez_compressed(OUT / "ridge_fit.npz", **rec)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["models"]:
+    if sys.argv[1:] == ["ridge_fit"]:
+        make_ridge_fit(_import_reference())
+    elif sys.argv[1:] == ["models"]:
         make_models(_import_reference())
     elif sys.argv[1:] == ["io"]:
         make_io(_import_reference())

@@ -141,3 +141,48 @@ def test_downstream_accuracy_within_half_point(ex):
     want = O.nn_predict(feats_dev[tr], labels[tr], feats_dev[te])
     got = P.classify.predict_many(model, P.CountFeatures(counts[idx_te], plan, enc), ex)
     assert np.mean(got == want) >= 0.98
+
+
+@gpu
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_ridge_fit_matches_reference(ex, golden, k):
+    """Ridge one-vs-all fit (classify.py:86-106) on the device: primal (k=0: n > d + 1), dual (k=1:
+    n <= d + 1) and explicit lambda (k=2) against the unmodified reference's weights and predictions."""
+    import paper_2209_13027_b200 as P
+
+    g = golden("ridge_fit")
+    lam_in = float(g[f"lam_in{k}"])
+    m = P.classify.fit(g[f"x{k}"], g[f"labels{k}"], kind="ridge_one_vs_all",
+                       lam=None if lam_in < 0 else lam_in, executor=ex)
+    assert m.lam == pytest.approx(float(g[f"lam{k}"]), rel=1e-13)
+    w = g[f"weights{k}"]
+    assert m.weights.shape == w.shape
+    assert np.linalg.norm(m.weights - w) <= 1e-9 * np.linalg.norm(w)
+    assert np.array_equal(P.classify.predict_many(m, g[f"q{k}"], executor=ex), g[f"pred{k}"])
+
+
+@gpu
+def test_ridge_fit_reproduces_reference_model_file(ex, golden):
+    """The reference's own ridge model (tests/golden/model_ridge.txt, fitted by classify.fit on the
+    pipeline_small features) refitted on the device: same weights, same predictions."""
+    from pathlib import Path
+
+    import paper_2209_13027_b200 as P
+    from paper_2209_13027_b200 import model_io as M
+
+    small = golden("pipeline_small")
+    art = M.load_model(Path(__file__).resolve().parent / "golden" / "model_ridge.txt")
+    m = P.classify.fit(small["features"][:, :20], small["labels"].astype(np.int64), kind="ridge_one_vs_all",
+                       executor=ex)
+    w = art.classifier.weights
+    assert np.linalg.norm(m.weights - w) <= 1e-9 * np.linalg.norm(w)
+    g = golden("ridge")
+    assert np.array_equal(P.classify.predict_many(m, g["queries"], executor=ex), g["pred"])
+
+
+@gpu
+def test_ridge_fit_rejects_bad_lambda(ex):
+    import paper_2209_13027_b200 as P
+
+    with pytest.raises(P.ConfigError):
+        P.classify.fit(np.ones((6, 3)), np.arange(6) % 2, kind="ridge_one_vs_all", lam=0.0, executor=ex)
