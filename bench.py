@@ -65,6 +65,28 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def compute_peaks(sm_mhz: float):
+    """FP32 / FP64 / TF32-tensor peaks: profiles/round2_peaks.json (tools/measure_peaks.py, measured on
+    this pool's B200 at its max clock) scaled to the clock the timed region ran at; else derived."""
+    sms = 148
+    out = {"ffma_tflops": sms * 128 * 2 * sm_mhz * 1e6 / 1e12, "dfma_tflops": sms * 64 * 2 * sm_mhz * 1e6 / 1e12,
+           "tf32_tflops": sms * 4096 * sm_mhz * 1e6 / 1e12, "source": "derived (148 SMs x per-clock rate x clock)"}
+    f = ROOT / "profiles" / "round2_peaks.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        # the issue-rate ceilings (256 FFMA / 128 DFMA flop per clock per SM) stay the denominators when a
+        # microbenchmark falls short of them (the DMMA path reaches 127 of 128 FP64 flop per clock)
+        for key, ceil in (("ffma", 256.0), ("dfma", 128.0)):
+            per_clk = max(ceil, d.get(f"{key}_flop_per_clk_per_sm") or 0.0)
+            out[f"{key}_tflops"] = sms * per_clk * sm_mhz * 1e6 / 1e12
+        if d.get("tf32_flop_per_clk_per_sm"):
+            out["tf32_tflops"] = sms * d["tf32_flop_per_clk_per_sm"] * sm_mhz * 1e6 / 1e12
+        out["source"] = ("max(issue ceiling, profiles/round2_peaks.json microbenchmark) flop per clock per SM for "
+                         "FFMA / DFMA, measured tcgen05 TF32 MMA rate (tc_probe) x 148 SMs x the median SM clock "
+                         f"{sm_mhz:.0f} MHz of the timed region")
+    return out
+
+
 # ---------------------------------------------------------------------------- clocks
 
 class ClockSampler:
@@ -190,6 +212,21 @@ def cpu_reference(workload: str, n_img: int, threads: int, reps: int = 1, warm: 
     return rates, sample
 
 
+def cpu_baseline(workload: str, sample: int, reps: int = 3):
+    """The reference algorithm on this box's host cores: all cores (one sample batch
+    per thread, median of `reps`) and one thread (one batch, the reference's run_bench pinning)."""
+    threads = os.cpu_count() or 1
+    rates, desc = cpu_reference(workload, sample, threads, reps=reps)
+    one_n = max(4, min(16, sample // 4))
+    one, one_desc = cpu_reference(workload, one_n, 1, reps=1)
+    return {"value": statistics.median(rates), "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": desc, "runs": rates, "median_of": len(rates),
+            "one_thread": {"value": one[0], "unit": "images/s", "cores": 1, "sample": one_desc},
+            "note": "oracle/ is a numpy restatement of the reference's calls (same numpy/BLAS operations, pinned to "
+                    "golden vectors of the unmodified reference); profiles/round2_port_vs_reference.json times it "
+                    "against the unmodified reference on one sample"}
+
+
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
@@ -197,6 +234,8 @@ def run_reference(args, rank: int, world: int):
     n_img = min(args.cpu_sample, 64)
     rates, sample = cpu_reference(args.workload, n_img, threads, reps=args.steps, warm=args.warmup)
     v = statistics.median(rates)
+    one_n = max(4, min(16, n_img // 4))
+    one, one_desc = cpu_reference(args.workload, one_n, 1, reps=1)
     from paper_2209_13027_b200 import synthetic
 
     cfg = synthetic.CONFIGS[args.workload]
@@ -207,7 +246,9 @@ def run_reference(args, rank: int, world: int):
         "config": {"workload": args.workload, "images": cfg["m"], "sample_images": n_img,
                    "image": [cfg["p"], cfg["q"]], "classes": cfg["classes"], "layers": cfg["layers"],
                    "block": cfg["block"]},
-        "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port", "sample": sample,
+                         "runs": rates, "one_thread": {"value": one[0], "unit": "images/s", "cores": 1,
+                                                       "sample": one_desc}},
         "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -312,7 +353,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         w = dict(eng.work.get(name) or {})
         if w.get("calls"):
             # per-launch algorithmic work = total over the timed steps / launches
-            for key in ("flops", "bytes", "gram_flops"):
+            for key in ("flops", "bytes", "gram_flops", "tensor_flops"):
                 if key in w:
                     w[key] = w[key] / w["calls"]
         kern[name] = {"ms_avg": sum(times) / len(times), "launches": len(times),
@@ -395,41 +436,65 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank != 0:
         return
     pk, pk_kind = peaks()
-    # roofline of the dominant kernel
-    roof = None
-    if kern:
-        top = max(kern, key=lambda k: kern[k]["ms_per_step"])
-        k = kern[top]
+    sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    cp = compute_peaks(sm_mhz)
+
+    def kernel_roofline(name):
+        k = kern[name]
         w = k["work"] or {}
-        sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
-        if w.get("kind") == "fma":
-            peak_tf = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-            ach = w["flops"] / (k["ms_avg"] / 1e3) / 1e12
-            roof = {"kernel": top, "bound": "fp32_fma", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": ach / peak_tf, "traffic": None,
-                    "peak_note": f"148 SMs x 128 FFMA/clk x 2 x median SM clock {sm_mhz} MHz (derived; "
-                                 "microbench measured 71.5 TFLOP/s at 1965 MHz)",
-                    "hbm_achieved_gbs": w["bytes"] / (k["ms_avg"] / 1e3) / 1e9,
-                    "hbm_peak_gbs": pk["hbm_gbs"], "share_of_step": k["ms_per_step"] / ms}
+        if not w.get("flops") and not w.get("bytes"):
+            return None
+        t = k["ms_avg"] / 1e3
+        ach = w.get("flops", 0.0) / t / 1e12
+        r = {"kernel": name, "share_of_step": k["ms_per_step"] / ms, "ms_per_launch": k["ms_avg"]}
+        if w.get("kind") == "tensor":
+            # algorithmic flops = the convolution's own 2 * taps * filters per pixel (single pass);
+            # executed = what the tensor pipe ran (3xTF32 split products, banded B of K = 16 per tap row)
+            ex_tf = w.get("tensor_flops", 0.0) / t / 1e12
+            r.update({"bound": "tensor", "achieved": ach, "peak": cp["tf32_tflops"], "unit": "TFLOP/s",
+                      "frac": ach / cp["tf32_tflops"], "executed_tflops": ex_tf,
+                      "tensor_pipe_frac": ex_tf / cp["tf32_tflops"], "vs_ffma_peak": ach / cp["ffma_tflops"],
+                      "note": "tcgen05 kind::tf32, 3xTF32 (3 MMAs per product) x banded B (16 K columns per "
+                              "7 taps): executed = 6.9x algorithmic at 7x7; vs_ffma_peak = algorithmic rate over "
+                              "the FP32 CUDA-core peak the FFMA kernel is capped by"})
+        elif w.get("kind") == "fma":
+            r.update({"bound": "fp32_fma", "achieved": ach, "peak": cp["ffma_tflops"], "unit": "TFLOP/s",
+                      "frac": ach / cp["ffma_tflops"]})
         elif w.get("kind") == "fp64":
-            peak_tf = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
-            ach = w["flops"] / (k["ms_avg"] / 1e3) / 1e12
-            roof = {"kernel": top, "bound": "fp64_fma", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": ach / peak_tf, "traffic": None, "share_of_step": k["ms_per_step"] / ms}
-    # DDCCA statistics in the full-GEMM convention (2 views x 2 d^2 per patch)
-    # against the dense TF32 tensor peak a 3xTF32 tcgen05 Gram would run on
+            r.update({"bound": "fp64_fma", "achieved": ach, "peak": cp["dfma_tflops"], "unit": "TFLOP/s",
+                      "frac": ach / cp["dfma_tflops"]})
+        elif w.get("kind") == "hbm":
+            gbs = w["bytes"] / t / 1e9
+            r.update({"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                      "frac": gbs / pk["hbm_gbs"]})
+        if w.get("bytes"):
+            r["hbm_achieved_gbs"] = w["bytes"] / t / 1e9
+            r["hbm_peak_gbs"] = pk["hbm_gbs"]
+        return r
+
+    rooflines = {n: r for n in kern for r in [kernel_roofline(n)] if r is not None}
+    roof = None
+    if rooflines:
+        top = max(rooflines, key=lambda n: kern[n]["ms_per_step"])
+        roof = dict(rooflines[top])
+        roof["traffic"] = None
+    # DDCCA statistics in the full-GEMM convention (2 views x 2 d^2 per patch), i.e. the
+    # work a 3xTF32 tcgen05 Gram would do: a GEMM-equivalent rate, not tensor-pipe use (the exact lag
+    # form runs on the FP64 pipe and uses no tensor cores)
     gram = None
     mom = [k for k in kern if k.startswith("moments_l") and (kern[k]["work"] or {}).get("gram_flops")]
     if mom:
         gfl = sum(kern[k]["work"]["gram_flops"] * kern[k]["launches"] / args.steps for k in mom)
         gms = sum(kern[k]["ms_per_step"] for k in mom)
-        tf32 = pk.get("bf16_tflops", 1649.0) / 2.0
+        tf32 = cp["tf32_tflops"]
         ach = gfl / (gms / 1e3) / 1e12
-        gram = {"kernels": mom, "gemm_equiv_flop_per_step": gfl, "ms_per_step": gms, "achieved_tflops": ach,
-                "tf32_dense_peak_tflops": tf32, "frac_of_tf32_peak": ach / tf32,
-                "frac_of_3xtf32_ceiling": ach / (tf32 / 3.0),
-                "note": "exact FP64 lag form (85 DFMA/pixel at 7x7) instead of a 3xTF32 Gram (2 d^2 = 4802 "
-                        "flop/patch); TF32 dense peak = measured bf16 / 2"}
+        gram = {"kernels": mom, "gemm_equiv_flop_per_step": gfl, "ms_per_step": gms,
+                "gemm_equiv_tflops": ach, "tf32_dense_peak_tflops": tf32,
+                "gemm_equiv_frac_of_tf32_peak": ach / tf32, "gemm_equiv_frac_of_3xtf32_ceiling": ach / (tf32 / 3.0),
+                "tensor_pipe_used": False,
+                "note": "GEMM-equivalent bookkeeping: the exact FP64 lag form (85 DFMA per pixel at 7x7) does the "
+                        "statistics a 3xTF32 Gram (2 d^2 = 4802 flop per patch) would; this is the Gram-convention "
+                        "rate, the tensor pipe is idle in these kernels"}
     if roof is not None:
         # DRAM bytes per launch of the same kernel from the committed ncu launch list
         tf = ROOT / "profiles" / "traffic.json"
@@ -447,10 +512,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     roof["algorithmic_bytes"] = w["bytes"]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        threads = os.cpu_count() or 1
-        rates, sample = cpu_reference(args.workload, args.cpu_sample, threads)
-        cpu = {"value": statistics.median(rates), "unit": "images/s", "cores": threads, "kind": "port",
-               "sample": sample}
+        cpu = cpu_baseline(args.workload, args.cpu_sample)
     line = {
         "metric": "images/sec fit+transform", "value": value, "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -464,7 +526,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                    "deterministic": bool(args.deterministic)},
         "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "gram": gram,
         "downstream": downstream,
-        "kernels": kern, "peaks_source": pk_kind,
+        "kernels": kern, "rooflines": rooflines, "peaks_source": pk_kind, "compute_peaks": cp,
     }
     print(json.dumps(line), flush=True)
 

@@ -203,6 +203,9 @@ DDCCA_API int ddcca_conv_hw(const float* in, int64_t n_maps, const ddcca_geom* g
 DDCCA_API int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack_host,
                                  int count, int center, int block_h, int block_w, void* counts, int count_kind,
                                  int64_t groups_per_row, int64_t row_stride, int64_t group_stride, void* stream);
+/* Which kernel the calling thread's last ddcca_conv_hist_* call launched: 1 = tcgen05 tensor
+ * cores (3xTF32), 0 = FFMA. For roofline accounting. */
+DDCCA_API int ddcca_conv_hist_last_path(void);
 DDCCA_API int ddcca_conv_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,
                              int count, int center, float* out, void* stream);
 DDCCA_API int ddcca_conv_hist_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,

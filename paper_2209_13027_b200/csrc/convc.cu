@@ -588,6 +588,8 @@ using namespace ddcca;
 
 namespace {
 
+thread_local int g_last_hist_path = 0;  // 1: the last conv-histogram launch ran on the tensor cores
+
 int conv_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* pack, bool pack_dev, int count,
                int center, float* out, void* stream) {
   Geo g{};
@@ -617,6 +619,7 @@ int conv_hist_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const
   if (!pack) return fail(DDCCA_ESHAPE, "null taps");
   if (n_maps == 0) return DDCCA_OK;
   cudaStream_t st = as_stream(stream);
+  g_last_hist_path = 0;
   CArgs A{};
   A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
   A.count = count; A.center = center & 1; A.responses = (center & DDCCA_CONV_RESPONSES) ? 1 : 0; A.out = nullptr;
@@ -636,7 +639,10 @@ int conv_hist_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const
         return fail(DDCCA_ECUDA, "tap stage symbol");
       DDCCA_TRY(stage_taps(pack, pack_dev, count, g.d, TC_FILTERS, A.center, false, st));
       const int rc = conv_hist_tc(t, stage, st);
-      if (rc != DDCCA_ECONFIG) return rc;
+      if (rc != DDCCA_ECONFIG) {
+        g_last_hist_path = rc == DDCCA_OK ? 1 : 0;
+        return rc;
+      }
     }
   }
   return dispatch<true>(A, g.l1, g.l2, pack, pack_dev, st);
@@ -662,6 +668,8 @@ int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, co
   return conv_hist_entry(in, n_maps, gg, conv_pack_host, false, count, center, block_h, block_w, counts, count_kind,
                          groups_per_row, row_stride, group_stride, stream);
 }
+
+int ddcca_conv_hist_last_path(void) { return g_last_hist_path; }
 
 int ddcca_conv_hist_dev(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack, int count,
                         int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,

@@ -560,10 +560,14 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
       // convert each landed float32 stage once into a float64 tile shared by all consumer
       // warps (every element is read by ~l2 + 2 threads: one conversion instead of one
       // F2F per read on the FP64 pipe), release the float32 slot, then run the rings on doubles
-      double* t64 = reinterpret_cast<double*>(empty + NS);  // 16-byte aligned: 2 NS barriers after the stages
+      // Two float64 tiles: stage s converts into tile s & 1 while no consumer can still be
+      // reading it (tile s & 1 last served stage s - 2, and every warp finished that stage's
+      // maps before it reached stage s - 1's barrier), so one barrier per stage suffices.
+      double* t64b = reinterpret_cast<double*>(empty + NS);  // 16-byte aligned: 2 NS barriers after the stages
       const int ctid = threadIdx.x, cthreads = G * 32;
       for (int s = 0; s < nstages; ++s) {
         const int slot = s % NS;
+        double* t64 = t64b + (s & 1) * max_stage;
         mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
         const float* tile = stage_mem + slot * max_stage;
         const int64_t ms = ma + (int64_t)s * mb;
@@ -578,7 +582,6 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
         if (lane == 0) mbar_arrive(&empty[slot]);
         for (int j = 0; j < nm; ++j)
           lag_map<L1, TCB>(t64 + j * tile_elems, TCB, nrows, cown, cpart, short_task, skip0, kk, acc);
-        consumer_sync(cthreads);  // t64 is rewritten by the next stage
       }
     } else {
       for (int s = 0; s < nstages; ++s) {
@@ -1338,8 +1341,11 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
             ((size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb + 31) / 32 * 32;
         bx.f64 = env_int("DDCCA_LAG_F32", 0) == 0 ? 1 : 0;
         bx.f32blocks = (flags & DDCCA_MOMENTS_F32_BLOCKS) ? 1 : 0;
+        // float64 path: two compute tiles (one barrier per stage) and, by default, two float32
+        // TMA stages, so two CTAs still fit one SM
+        if (bx.f64 && !bx.f32blocks) bx.ns = std::max(2, std::min(8, env_int("DDCCA_TMA_STAGES", 2)));
         const size_t tsmem = sizeof(float) * bx.ns * max_stage + (2 * bx.ns + 1) * sizeof(uint64_t) +
-                             (bx.f64 ? sizeof(double) * max_stage : 0);
+                             (bx.f64 ? 2 * sizeof(double) * max_stage : 0);
         dim3 tblock(32 * (P.G + 1));
         // task ids by kind, uploaded after the plan tables
         std::vector<int> ids_int, ids_short;

@@ -607,9 +607,18 @@ class Engine:
                     nb_cols = plan.nbx * plan.bw
                     fl_f = 2.0 * n * plan.nby * plan.bh * nb_cols * last.count * last.geom.dim
                     by_f = 4.0 * n * pp * qq + n * plan.blocks * plan.bins * out.element_size()
-                    if self._timed("conv_hist", 1, {"kind": "fma", "flops": fl_f, "bytes": by_f}, conv_hist, ex, maps,
-                                   last, view, plan, base, kind, groups, featlen, plan.blocks * plan.bins,
-                                   len(layers) > 1):
+                    wk = {"kind": "fma", "flops": fl_f, "bytes": by_f}
+                    if self._timed("conv_hist", 1, wk, conv_hist, ex, maps, last, view, plan, base, kind, groups,
+                                   featlen, plan.blocks * plan.bins, len(layers) > 1):
+                        if lib.ddcca_conv_hist_last_path() == 1 and self.profile is not None:
+                            # tcgen05 3xTF32 kernel (convtc.cu): 3 MMAs M128 x N(8 filters x 8 columns) x K8
+                            # per tap row and 8-column K chunk, 2 chunks per 8 output columns, 128-row tiles
+                            blocks = -(-nb_cols // 8)
+                            tiles = -(-pp // 128)
+                            ex_fl = 2.0 * 128 * 64 * 8 * 3 * 2 * last.geom.l1 * blocks * tiles * n
+                            acc = self.work["conv_hist"]
+                            acc["kind"] = "tensor"
+                            acc["tensor_flops"] = acc.get("tensor_flops", 0.0) + ex_fl
                         continue
                     codes = self._timed("conv_hash", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv_hash, ex,
                                         maps, last, view)
