@@ -413,15 +413,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
         for _ in range(max(1, min(2, args.warmup))):
             e2e_step()
-        ex.synchronize()
+        torch.cuda.synchronize()
         barrier()
+        # timed on the caller's (current) stream: compute_feature_counts orders it after the
+        # executor's kernels AND the streamed device->host copies of every step, while the
+        # executor's stream runs ahead into the next step's upload + fit (steps pipeline over
+        # PCIe: step k's counts download while step k+1's images upload)
+        cur = torch.cuda.current_stream(dev)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
-        a.record(ex.stream)
+        a.record(cur)
         for _ in range(args.steps):
             e2e_step()
-        b.record(ex.stream)
+        cur.wait_stream(ex.stream)
+        b.record(cur)
         b.synchronize()
         wall = (time.perf_counter() - t0) / args.steps
         ms_e = max(a.elapsed_time(b) / args.steps, wall * 1000.0)

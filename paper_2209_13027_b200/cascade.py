@@ -280,10 +280,16 @@ def _upload_chunked(ex, h1, h2, rows_per_chunk: int):
     import torch
 
     m = h1.shape[0]
-    d1 = torch.empty(h1.shape, dtype=torch.float32, device=ex.device)
-    d2 = torch.empty(h2.shape, dtype=torch.float32, device=ex.device)
-    up = torch.cuda.Stream(device=ex.device)
-    up.wait_stream(ex.stream)  # the fresh buffers' memory may still be in use by earlier work
+    up = getattr(ex, "upload_stream", None)
+    if up is None:
+        up = ex.upload_stream = torch.cuda.Stream(device=ex.device)
+    # Buffers are allocated on the executor's persistent upload stream and marked as used by
+    # the compute stream: the caching allocator then never hands this step's upload a block
+    # that earlier compute work may still read, so the upload need not wait for the compute
+    # stream -- the next fit's images stream in while the previous transform still runs.
+    with torch.cuda.stream(up):
+        d1 = torch.empty(h1.shape, dtype=torch.float32, device=ex.device)
+        d2 = torch.empty(h2.shape, dtype=torch.float32, device=ex.device)
     events = []
     with torch.cuda.stream(up):
         for r0 in range(0, m, max(1, rows_per_chunk)):
@@ -293,8 +299,8 @@ def _upload_chunked(ex, h1, h2, rows_per_chunk: int):
             ev = torch.cuda.Event()
             ev.record(up)
             events.append((r1, ev))
-    d1.record_stream(up)
-    d2.record_stream(up)
+    d1.record_stream(ex.stream)
+    d2.record_stream(ex.stream)
     return d1, d2, events
 
 

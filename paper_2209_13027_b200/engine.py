@@ -330,6 +330,7 @@ class Engine:
         self.profile = None   # dict name -> [(start_event, end_event)] when profiling
         self.work = {}        # name -> algorithmic work of one call (for the roofline)
         self.launches = 0     # kernels launched by this engine
+        self.host_copy_done = None  # event of the last streamed device->host count copy
 
     def _timed(self, name: str, kernels: int, work: dict | None, fn, *a, **k):
         torch = _torch()
@@ -563,7 +564,11 @@ class Engine:
         """(m, p, q) x2 -> per-sample block counts (m, featlen) u8/u16 on device.
 
         ``host_out`` (pinned host tensor of the same shape): each super-batch's counts
-        are copied out on a side stream while the next super-batch is computed.
+        are copied out on a side stream while the next super-batch is computed. The
+        executor's stream does NOT wait for those copies (the next fit can start while the
+        counts still stream out over PCIe); ``self.host_copy_done`` is the event that
+        completes with the last copy (pipeline.compute_feature_counts hands it to the
+        caller's stream).
         ``sink(s0, s1, counts)``: streaming consumer; the device buffer then holds
         one super-batch only (for outputs larger than HBM, e.g. the 3-stage config)
         and the returned tensor is that rolling buffer.
@@ -638,7 +643,10 @@ class Engine:
                 if sink is not None:
                     sink(s0, s1, out[:s1 - s0])
             if copy_stream is not None:
-                ex.stream.wait_stream(copy_stream)
+                # the device buffer stays allocated until the copy stream is done with it
+                out.record_stream(copy_stream)
+                self.host_copy_done = torch.cuda.Event()
+                self.host_copy_done.record(copy_stream)
         return out, plan
 
     def expand(self, counts, plan: BlockPlan, enc):

@@ -65,6 +65,7 @@ class Executor:
         self.device = torch.device("cuda", device) if not isinstance(device, torch.device) else device
         torch.cuda.set_device(self.device)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        self.upload_stream = None  # created by the first chunked (pinned) image upload
         self.group = process_group
         dist = torch.distributed
         if dist.is_available() and dist.is_initialized():

@@ -55,7 +55,11 @@ def compute_feature_counts(ds, bank, config, executor=None, host_out=None):
     World size 1: all samples. With a process group, the rank's batch shard
     (the same contiguous shard train_network used), rows [s0, s1) of the
     dataset. ``host_out``: optional pinned host tensor; counts are streamed into
-    it super-batch by super-batch while the transform proceeds.
+    it super-batch by super-batch while the transform proceeds. The caller's
+    current stream is ordered after those copies (synchronize it, or the device,
+    before reading ``host_out``); the executor's stream is not, so a following fit
+    overlaps the tail of the copies (PCIe is full duplex: the next upload and
+    this download share no direction).
     """
     import torch
 
@@ -81,6 +85,8 @@ def compute_feature_counts(ds, bank, config, executor=None, host_out=None):
             i2 = _to_dev32(ex, v2[s0:s1])
         counts, plan = eng.transform_counts(i1, i2, layers, enc, bs, host_out=host_out)
     handoff(ex, counts)
+    if host_out is not None and eng.host_copy_done is not None:
+        torch.cuda.current_stream(ex.device).wait_event(eng.host_copy_done)
     return counts, plan
 
 
