@@ -45,9 +45,9 @@ constexpr int N = NF * X;                  // MMA N
 constexpr int NA = 3;                      // TMEM ring of A slots
 constexpr int NS = 8;                      // SMEM ring of staged slots
 constexpr int RP = 136;                    // staged rows per slot: 128 lanes + halo (l <= 9)
-constexpr int EPI_WARPS = 4;               // warps 0..3: TMEM lane quadrants 0..3
-constexpr int MMA_WARP0 = 4, MMA_WARPS = 2;    // alternate column blocks (one accumulator each)
-constexpr int PROD_WARP0 = 6, PROD_WARPS = 4;  // one per TMEM lane quadrant
+constexpr int EPI_WARPS = 8;                   // warps 0..7: lane quadrant w % 4, accumulator w / 4
+constexpr int MMA_WARP0 = 8, MMA_WARPS = 2;    // alternate column blocks (one accumulator each)
+constexpr int PROD_WARP0 = 10, PROD_WARPS = 4; // one per TMEM lane quadrant
 constexpr int THREADS = 32 * (EPI_WARPS + MMA_WARPS + PROD_WARPS);
 constexpr int CHUNK_BYTES = RP * 16;       // 4 columns x RP rows
 constexpr int RAW_BYTES = 2 * CHUNK_BYTES; // one staged slot: 8 columns
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&dfull[i], 1);
-      mbar_init(&dempty[i], EPI_WARPS);
+      mbar_init(&dempty[i], EPI_WARPS / 2);  // the four epilogue warps of that accumulator
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -278,39 +278,51 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
-    const int y = 32 * warp + lane;  // map row of this lane (maps of <= 128 rows)
+    // Two groups of four warps, one per accumulator (column-block parity): each group
+    // reads its accumulator while the other group's block is still being multiplied.
+    const int q = warp & 3, grp = warp >> 2;
+    const int y = 32 * q + lane;  // map row of this lane (maps of <= 128 rows)
     const bool row_ok = y < rows;
     unsigned* rbins = bins + (row_ok ? (y / A.bh) * A.nbx * words : 0);
-    uint32_t blk = 0;
+    uint32_t use = 0;
     for (int64_t m = blockIdx.x; m < A.n_maps; m += gridDim.x) {
-      for (int c = 0; c < C; ++c, ++blk) {
-        const uint32_t db = blk & 1;
-        mbar_wait(&dfull[db], (blk >> 1) & 1);
+      const uint32_t b0 = (uint32_t)((m - blockIdx.x) / gridDim.x) * C;  // global block index of column 0
+      for (int c = 0; c < C; ++c) {
+        if (((b0 + c) & 1) != (uint32_t)grp) continue;
+        mbar_wait(&dfull[grp], use & 1);
+        ++use;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         uint32_t v0[32], v1[32];
-        const uint32_t ta = tm + ((uint32_t)(32 * warp) << 16) + dcol0 + db * N;
+        const uint32_t ta = tm + ((uint32_t)(32 * q) << 16) + dcol0 + grp * N;
         ld32(ta, v0);
         ld32(ta + 32, v1);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dempty[db]);
-        if (row_ok) {
-          // block column of the first pixel, then stepped (no per-pixel division)
-          int bx = (X * c) / A.bw, rem = X * c - bx * A.bw;
+        if (lane == 0) mbar_arrive(&dempty[grp]);
+        if (!row_ok) continue;
+        // sign bits -> LSB-first code; column n = f * X + xo: filters 0..3 in v0, 4..7 in v1
+        unsigned code[X];
+#pragma unroll
+        for (int xo = 0; xo < X; ++xo) {
+          unsigned cd = 0;
+#pragma unroll
+          for (int f = 0; f < NF; ++f)
+            if (__uint_as_float(f < 4 ? v0[f * X + xo] : v1[(f - 4) * X + xo]) > 0.f) cd |= 1u << f;
+          code[xo] = cd;
+        }
+        const int x0 = X * c;
+        const int bx0 = x0 / A.bw, rem0 = x0 - bx0 * A.bw;
+        if (x0 + X <= cols && rem0 + X <= A.bw) {
+          // all eight pixels inside one histogram block
+          unsigned* bb = rbins + bx0 * words;
+#pragma unroll
+          for (int xo = 0; xo < X; ++xo) atomicAdd(&bb[code[xo] >> 1], 1u << ((code[xo] & 1u) << 4));
+        } else {
+          int bx = bx0, rem = rem0;
 #pragma unroll
           for (int xo = 0; xo < X; ++xo) {
-            const int x = X * c + xo;
-            if (x < cols) {
-              // column n = f * X + xo: filters 0..3 in v0, 4..7 in v1
-              unsigned code = 0;
-#pragma unroll
-              for (int f = 0; f < NF; ++f) {
-                const uint32_t r = f < 4 ? v0[f * X + xo] : v1[(f - 4) * X + xo];
-                code |= (__uint_as_float(r) > 0.f ? 1u : 0u) << f;
-              }
-              atomicAdd(&rbins[bx * words + (code >> 1)], 1u << ((code & 1u) << 4));
-            }
+            if (x0 + xo < cols) atomicAdd(&rbins[bx * words + (code[xo] >> 1)], 1u << ((code[xo] & 1u) << 4));
             if (++rem == A.bw) {
               rem = 0;
               ++bx;
@@ -320,7 +332,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
       }
       // the map's histograms are complete: counts into the feature row, bins cleared
       asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-      for (int b = warp; b < nblk; b += EPI_WARPS) {
+      for (int b = warp; b < nblk; b += EPI_WARPS) {  // all epilogue warps
         unsigned* wb = bins + b * words;
         const int64_t base = (m / A.gpr) * A.row_stride + (m % A.gpr) * A.group_stride + (int64_t)b * nbins;
         if (A.kind == 2) {
