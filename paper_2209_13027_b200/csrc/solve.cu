@@ -342,9 +342,102 @@ __device__ void matmul(const double* A, bool ta, const double* Bm, bool tb, doub
   __syncthreads();
 }
 
-// inv_sqrt (solver.py:161-170) into r; eigen scratch from the caller.
+// C = A B for dp x dp row-major matrices in shared memory (dp % 8 == 0), on the FP64 tensor
+// path: one warp per 8 x 8 output tile, mma.sync m8n8k4 f64 over K (each product and sum in
+// float64, like the FFMA form, at the DMMA pipe's rate instead of one load per DFMA).
+__device__ void gemm_dmma(const double* __restrict__ A, const double* __restrict__ Bm, double* __restrict__ C,
+                          int dp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = dp >> 3, r = lane >> 2, c4 = lane & 3;
+  for (int t = warp; t < nt * nt; t += blockDim.x >> 5) {
+    const int ti = t / nt, tj = t - ti * nt;
+    // two independent accumulator pairs (k = 0, 8, .. and k = 4, 12, ..) halve the
+    // dependent DMMA chain; dp % 8 == 0
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+    const double* arow = A + (ti * 8 + r) * dp + c4;  // A[8 ti + r][k + c4]
+    const double* bcol = Bm + c4 * dp + tj * 8 + r;   // B[k + c4][8 tj + r]
+#pragma unroll 2
+    for (int k = 0; k < dp; k += 8) {
+      const double a0 = arow[k], a1 = arow[k + 4];
+      const double b0 = bcol[k * dp], b1 = bcol[(k + 4) * dp];
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+          : "+d"(d0), "+d"(d1)
+          : "d"(a0), "d"(b0));
+      asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+          : "+d"(e0), "+d"(e1)
+          : "d"(a1), "d"(b1));
+    }
+    double* o = C + (ti * 8 + r) * dp + tj * 8 + 2 * c4;
+    o[0] = d0 + e0;
+    o[1] = d1 + e1;
+  }
+  __syncthreads();
+}
+
+constexpr int NS_MAX_DP = 64;    // coupled Newton-Schulz in shared memory up to 64 x 64 (padded)
+constexpr int NS_MAX_ITERS = 100;
+
+__host__ __device__ inline int ns_dp(int n) { return (n + 7) & ~7; }
+__host__ __device__ inline size_t ns_smem_doubles(int n) {
+  const size_t dp = (size_t)ns_dp(n);
+  return dp <= (size_t)NS_MAX_DP ? 4 * dp * dp : 0;
+}
+
+// Symmetric inverse square root of an SPD matrix by the coupled Newton-Schulz iteration
+// (Y0 = A / ||A||_F, Z0 = I; T = (3 I - Z Y) / 2, Y <- Y T, Z <- T Z; Z -> (A / ||A||_F)^-1/2),
+// padded with an identity block to a multiple of 8 for the DMMA tiles. The result is the
+// same matrix the reference's V diag(w^-1/2) V' (solver.py:161-170) computes, to rounding;
+// returns false (the caller then runs the Jacobi form, which also reports non-PD input) when
+// the iteration does not converge: not positive definite, or too ill-conditioned.
+__device__ bool ns_inv_sqrt(const double* c, int n, double* r, double* buf, Blk& B) {
+  const int dp = ns_dp(n), np = dp * dp;
+  double *Y = buf, *Z = buf + np, *T = buf + 2 * np, *W = buf + 3 * np;
+  double fro = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += c[e] * c[e];
+  fro = sqrt(block_sum(fro, B));
+  if (!(fro > 0.0) || !isfinite(fro)) return false;
+  const double inv = 1.0 / fro;
+  for (int e = threadIdx.x; e < np; e += blockDim.x) {
+    const int i = e / dp, j = e - i * dp;
+    Y[e] = (i < n && j < n) ? 0.5 * (c[i * n + j] + c[j * n + i]) * inv : (i == j ? 1.0 : 0.0);
+    Z[e] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int settled = 0;
+  for (int it = 0; it < NS_MAX_ITERS; ++it) {
+    gemm_dmma(Z, Y, T, dp);
+    double err = 0.0;
+    for (int e = threadIdx.x; e < np; e += blockDim.x) {
+      const int i = e / dp, j = e - i * dp;
+      const double t = (i == j ? 1.5 : 0.0) - 0.5 * T[e];
+      T[e] = t;
+      err = fmax(err, fabs(t - (i == j ? 1.0 : 0.0)));
+    }
+    err = block_max(err, B);  // includes the barrier before T is read
+    gemm_dmma(Y, T, W, dp);
+    double* x = Y; Y = W; W = x;
+    gemm_dmma(T, Z, W, dp);
+    x = Z; Z = W; W = x;
+    if (!(err < 1e30)) return false;  // diverging: not positive definite
+    // quadratic convergence: two more sweeps once the residual is small reach rounding level
+    if (err < 1e-11 && ++settled >= 3) {
+      const double s = rsqrt(fro);
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        r[e] = 0.5 * (Z[i * dp + j] + Z[j * dp + i]) * s;
+      }
+      __syncthreads();
+      return true;
+    }
+  }
+  return false;
+}
+
+// inv_sqrt (solver.py:161-170) into r; eigen scratch from the caller. nsbuf (shared memory,
+// ns_smem_doubles(n)) enables the Newton-Schulz form; Jacobi otherwise or as its fallback.
 __device__ int inv_sqrt_dev(const double* c, int n, double* r, double* w, double* v, double* a, double* va, double* cs,
-                            double* tmp, double* wtmp, Blk& B) {
+                            double* tmp, double* wtmp, Blk& B, double* nsbuf = nullptr) {
+  if (nsbuf != nullptr && ns_inv_sqrt(c, n, r, nsbuf, B)) return DDCCA_OK;
   int rc = sym_eig_dev(c, n, w, v, a, va, cs, tmp, wtmp, B);
   if (rc != DDCCA_OK) return rc;
   if (!(w[n - 1] > 0.0)) return DDCCA_ENUMERICAL;
@@ -503,92 +596,109 @@ __global__ void __launch_bounds__(SOLVE_THREADS) whiten_kernel(SolveArgs S) {
   __syncthreads();
   Blk B{red, &flag, iscr};
   const double* c = S.fin + (b == 0 ? 0 : nn);
-  const int rc = inv_sqrt_dev(c, n, b == 0 ? L.R1 : L.R2, lam, ev, ja, jva, cs, jtmp, wsc, B);
+  double* nsbuf = ns_smem_doubles(n) ? base + (S.jacobi_in_smem ? 2 * nn : 0) : nullptr;
+  const int rc = inv_sqrt_dev(c, n, b == 0 ? L.R1 : L.R2, lam, ev, ja, jva, cs, jtmp, wsc, B, nsbuf);
   if (rc != DDCCA_OK && threadIdx.x == 0) atomicCAS(reinterpret_cast<int*>(S.status), 0, rc);
 }
 
-__global__ void __launch_bounds__(SOLVE_THREADS) solve_kernel(SolveArgs S) {
+// ---- after the whitening: T = R1 C~ R2, G1 = T T', G2 = T' T (solver.py:230-247) --------------
+// dp x dp shared-memory tiles (zero padding is exact for these products) on the DMMA path; the
+// plain per-entry form above NS_MAX_DP.
+__device__ void load_padded(const double* src, int n, double* dst, int dp, bool transpose) {
+  for (int e = threadIdx.x; e < dp * dp; e += blockDim.x) {
+    const int i = e / dp, j = e - i * dp;
+    dst[e] = (i < n && j < n) ? (transpose ? src[j * n + i] : src[i * n + j]) : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(SOLVE_THREADS) gram_kernel(SolveArgs S) {
+  extern __shared__ double sm[];
+  if (*S.status != 0) return;
+  const int n = S.d, nn = n * n;
+  const SolveLayout Y = solve_layout(S.ws, n, false, nullptr);
+  double* ct = S.fin + 4 * nn;
+  const int dp = ns_dp(n);
+  if (dp <= NS_MAX_DP) {
+    const int np = dp * dp;
+    double *a = sm, *b = sm + np, *c = sm + 2 * np, *t = sm + 3 * np, *tt = sm + 4 * np;
+    load_padded(Y.R1, n, a, dp, false);
+    load_padded(ct, n, b, dp, false);
+    __syncthreads();
+    gemm_dmma(a, b, c, dp);               // R1 C~
+    load_padded(Y.R2, n, a, dp, false);
+    __syncthreads();
+    gemm_dmma(c, a, t, dp);               // T = R1 C~ R2
+    for (int e = threadIdx.x; e < np; e += blockDim.x) {
+      const int i = e / dp, j = e - i * dp;
+      tt[e] = t[j * dp + i];
+    }
+    __syncthreads();
+    gemm_dmma(t, tt, a, dp);              // T T'
+    gemm_dmma(tt, t, b, dp);              // T' T
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      Y.T[e] = t[i * dp + j];
+      Y.ev[e] = 0.5 * (a[i * dp + j] + a[j * dp + i]);  // symmetrized eig inputs (solver.py:232, :240)
+      Y.Gm[e] = 0.5 * (b[i * dp + j] + b[j * dp + i]);
+    }
+    return;
+  }
+  matmul(Y.R1, false, ct, false, Y.NB, n, n, n);   // R1 C~
+  matmul(Y.NB, false, Y.R2, false, Y.T, n, n, n);  // T
+  matmul(Y.T, false, Y.T, true, Y.U, n, n, n);     // T T'
+  matmul(Y.T, true, Y.T, false, Y.V, n, n, n);     // T' T
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    Y.ev[e] = 0.5 * (Y.U[e] + Y.U[j * n + i]);
+    Y.Gm[e] = 0.5 * (Y.V[e] + Y.V[j * n + i]);
+  }
+}
+
+// eig(T T') (CTA 0: lam, U) and eig(T' T) (CTA 1: lam2, NB -- the null-space completion
+// basis, used only when a requested sigma vanishes) in parallel.
+__global__ void __launch_bounds__(SOLVE_THREADS) eig2_kernel(SolveArgs S) {
   extern __shared__ double sm[];
   __shared__ double red[SOLVE_THREADS / 32 + 1];
   __shared__ int flag;
-  const int n = S.d, C = S.C, L = S.count;
-  const int nn = n * n;
-  if (S.prewhitened && *S.status != 0) return;
-  int* iscr = reinterpret_cast<int*>(sm);  // 2n+2 ints
-  double* cs = sm + (2 * n + 2 + 1) / 2 + 1;  // 2n+2 doubles: per-round rotations
+  if (*S.status != 0) return;
+  const int n = S.d, nn = n * n;
+  const int b = blockIdx.x;
+  int* iscr = reinterpret_cast<int*>(sm);
+  double* cs = sm + (2 * n + 2 + 1) / 2 + 1;
   double* base = cs + 2 * n + 2;
-  const SolveLayout Y = solve_layout(S.ws, n, S.jacobi_in_smem != 0, base);
-  double *ja = Y.ja, *jva = Y.jva, *jtmp = Y.jtmp, *R1 = Y.R1, *R2 = Y.R2, *T = Y.T, *Gm = Y.Gm, *U = Y.U,
-         *V = Y.V, *NB = Y.NB, *ev = Y.ev, *lam = Y.lam, *wsc = Y.wsc, *sig = Y.sig, *flip = Y.flip,
-         *lam2 = Y.lam2;
-  Blk B{red, &flag, iscr};
-  double* ct = S.fin + 4 * nn;
+  const SolveLayout Y = solve_layout(S.ws, n, false, nullptr);
+  double *ja, *jva, *jtmp, *wsc;
+  if (b == 0) {
+    ja = Y.ja; jva = Y.jva; jtmp = Y.jtmp; wsc = Y.wsc;
+  } else {
+    double* g = Y.side + solve_side_doubles(n);  // the second whitening CTA's scratch (free now)
+    ja = g; jva = g + nn; g += 2 * nn;
+    jtmp = g; g += nn;
+    g += nn + n;  // ev, lam of that layout (unused here)
+    wsc = g;
+  }
+  if (S.jacobi_in_smem) {
+    ja = base;
+    jva = base + nn;
+  }
   if (threadIdx.x == 0) flag = 0;
   __syncthreads();
-  int rc = DDCCA_OK;
-  if (!S.prewhitened) {
-    double* c11 = S.fin;
-    double* c22 = S.fin + nn;
-    if (threadIdx.x == 0) *S.status = 0;
-    __syncthreads();
-    // ---- finalize (moments.py:168-193); payload == nullptr: fin already holds finalized moments
-    if (S.payload != nullptr && !finalize_dev(S.payload, n, C, S.eps, S.fin, B, threadIdx.x, blockDim.x)) {
-      if (threadIdx.x == 0) *S.status = DDCCA_ENUMERICAL;
-      return;
-    }
-    // ---- whitening (solver.py:227-229)
-    rc = inv_sqrt_dev(c11, n, R1, lam, ev, ja, jva, cs, jtmp, wsc, B);
-    if (rc == DDCCA_OK) rc = inv_sqrt_dev(c22, n, R2, lam, ev, ja, jva, cs, jtmp, wsc, B);
-    if (rc != DDCCA_OK) {
-      if (threadIdx.x == 0) *S.status = rc;
-      return;
-    }
-  }
-  matmul(R1, false, ct, false, Gm, n, n, n);  // Gm = R1 ct
-  matmul(Gm, false, R2, false, T, n, n, n);   // T = R1 ct R2
-  matmul(T, false, T, true, Gm, n, n, n);     // Gm = T T^T
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
-    const int i = e / n, j = e - i * n;
-    if (i <= j) {
-      const double x = 0.5 * (Gm[e] + Gm[j * n + i]);
-      ev[e] = x;
-      ev[j * n + i] = x;
-    }
-  }
-  __syncthreads();
-  rc = sym_eig_dev(ev, n, lam, U, ja, jva, cs, jtmp, wsc, B);
-  if (rc != DDCCA_OK) {
-    if (threadIdx.x == 0) *S.status = rc;
-    return;
-  }
+  Blk B{red, &flag, iscr};
+  const int rc = b == 0 ? sym_eig_dev(Y.ev, n, Y.lam, Y.U, ja, jva, cs, jtmp, wsc, B)
+                        : sym_eig_dev(Y.Gm, n, Y.lam2, Y.NB, ja, jva, cs, jtmp, wsc, B);
+  if (rc != DDCCA_OK && threadIdx.x == 0) atomicCAS(reinterpret_cast<int*>(S.status), 0, rc);
+}
+
+// sigma, right vectors with null-space completion, W1 = R1 U, W2 = R2 V, the shared sign
+// flips and the float32 conv packs (solver.py:233-257, :260-272).
+__global__ void __launch_bounds__(SOLVE_THREADS) finish_kernel(SolveArgs S) {
+  if (*S.status != 0) return;
+  const int n = S.d, L = S.count;
+  const SolveLayout Y = solve_layout(S.ws, n, false, nullptr);
+  double *R1 = Y.R1, *R2 = Y.R2, *T = Y.T, *U = Y.U, *V = Y.V, *NB = Y.NB, *lam = Y.lam, *sig = Y.sig,
+         *flip = Y.flip;
   for (int i = threadIdx.x; i < n; i += blockDim.x) sig[i] = sqrt(fmax(lam[i], 0.0));
   __syncthreads();
-  // ---- right vectors, null-space completion (solver.py:235-247)
-  __shared__ int need_null;
-  if (threadIdx.x == 0) {
-    need_null = 0;
-    const double thr = 1e-12 * fmax(sig[0], 1e-300);
-    for (int k = 0; k < L; ++k)
-      if (!(sig[k] > thr)) need_null = 1;
-  }
-  __syncthreads();
-  if (need_null) {
-    matmul(T, true, T, false, Gm, n, n, n);  // T^T T
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
-      const int i = e / n, j = e - i * n;
-      if (i <= j) {
-        const double x = 0.5 * (Gm[e] + Gm[j * n + i]);
-        ev[e] = x;
-        ev[j * n + i] = x;
-      }
-    }
-    __syncthreads();
-    rc = sym_eig_dev(ev, n, lam2, NB, ja, jva, cs, jtmp, wsc, B);
-    if (rc != DDCCA_OK) {
-      if (threadIdx.x == 0) *S.status = rc;
-      return;
-    }
-  }
   // column k of V (n x L row-major)
   __shared__ int null_src[64];
   if (threadIdx.x == 0) {
@@ -688,7 +798,8 @@ __global__ void __launch_bounds__(SOLVE_THREADS) sym_eig_kernel(EigArgs E) {
   if (E.mode == 0) {
     rc = sym_eig_dev(E.s, n, E.w, E.v, ja, jva, cs, jtmp, wsc, B);
   } else {
-    rc = inv_sqrt_dev(E.s, n, E.v, E.w, vv, ja, jva, cs, jtmp, wsc, B);
+    double* nsbuf = ns_smem_doubles(n) ? base + (E.jacobi_in_smem ? 2 * nn : 0) : nullptr;
+    rc = inv_sqrt_dev(E.s, n, E.v, E.w, vv, ja, jva, cs, jtmp, wsc, B, nsbuf);
   }
   if (threadIdx.x == 0) *E.status = rc;
 }
@@ -701,6 +812,8 @@ static size_t jacobi_smem(int n, bool in_smem) {
   size_t ints = sizeof(double) * ((2 * n + 2 + 1) / 2 + 1 + 2 * n + 2);
   return ints + (in_smem ? sizeof(double) * 2 * (size_t)n * n : 0);
 }
+// whitening / inv_sqrt kernels: the Jacobi area plus the Newton-Schulz buffers
+static size_t whiten_smem(int n, bool in_smem) { return jacobi_smem(n, in_smem) + sizeof(double) * ns_smem_doubles(n); }
 
 }  // namespace ddcca
 
@@ -733,10 +846,16 @@ int ddcca_solve(const double* payload, int dim, int class_count, double epsilon,
   } else {
     cudaMemsetAsync(status, 0, sizeof(int32_t), st);
   }
-  cudaFuncSetAttribute(whiten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  whiten_kernel<<<2, SOLVE_THREADS, sm, st>>>(S);
-  cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  solve_kernel<<<1, SOLVE_THREADS, sm, st>>>(S);
+  const size_t smw = whiten_smem(dim, in_smem);
+  cudaFuncSetAttribute(whiten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+  whiten_kernel<<<2, SOLVE_THREADS, smw, st>>>(S);
+  // T and both Grams (DMMA), then eig(T T') and eig(T' T) in parallel CTAs, then the filters
+  const size_t smg = ns_dp(dim) <= NS_MAX_DP ? sizeof(double) * 5 * (size_t)ns_dp(dim) * ns_dp(dim) : 0;
+  cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smg);
+  gram_kernel<<<1, SOLVE_THREADS, smg, st>>>(S);
+  cudaFuncSetAttribute(eig2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  eig2_kernel<<<2, SOLVE_THREADS, sm, st>>>(S);
+  finish_kernel<<<1, SOLVE_THREADS, 0, st>>>(S);
   return check_launch("solve_kernel");
 }
 
@@ -753,7 +872,7 @@ int ddcca_sym_eig(const double* s, int n, int mode, double* w, double* v, int32_
   if (n < 1) return fail(DDCCA_ESHAPE, "expected a square matrix");
   if (ws_bytes < ddcca_solve_workspace(n)) return fail(DDCCA_ECONFIG, "eig workspace too small");
   const bool in_smem = n <= SMEM_JACOBI_MAX_N;
-  const size_t sm = jacobi_smem(n, in_smem);
+  const size_t sm = mode == 1 ? whiten_smem(n, in_smem) : jacobi_smem(n, in_smem);
   EigArgs E{s, n, mode, w, v, status, static_cast<double*>(ws), in_smem ? 1 : 0};
   cudaFuncSetAttribute(sym_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   sym_eig_kernel<<<1, SOLVE_THREADS, sm, as_stream(stream)>>>(E);
