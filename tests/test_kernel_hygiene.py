@@ -1,0 +1,166 @@
+"""Race and out-of-bounds evidence for the device kernels without compute-sanitizer (GPU).
+
+compute-sanitizer is closed on this GPU pool (runs under it left GPUs needing a
+reset), so the kernels are checked the way the pool suggests instead:
+
+* repetition determinism: every kernel family runs several times on the same
+  inputs and must produce bit-identical outputs. The kernels whose results do
+  not depend on scheduling by construction (fixed reduction orders, integer
+  shared-memory histograms, TMA/mbarrier rings) would show a shared-memory race
+  or a missing barrier as run-to-run differences;
+* guard bands: every output buffer is allocated with a 64 KB margin on both
+  sides filled with a sentinel; the margins must be intact afterwards (an
+  out-of-bounds store anywhere near an output is caught);
+* small and ragged shapes (maps smaller than the window, widths not a multiple
+  of 4, the cp.async staging path, single batches) against the CPU oracle.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2209_13027_b200 as P  # noqa: E402
+from paper_2209_13027_b200 import _native  # noqa: E402
+from paper_2209_13027_b200 import engine as E  # noqa: E402
+
+GUARD = 1 << 16
+SENTINEL = 0xA5
+
+
+@pytest.fixture(scope="module")
+def ex():
+    return P.Executor(P.ExecSettings())
+
+
+class Guarded:
+    """A device tensor view with sentinel-filled margins on both sides."""
+
+    def __init__(self, shape, dtype, device):
+        self.numel = int(np.prod(shape))
+        esz = torch.empty((), dtype=dtype).element_size()
+        nbytes = self.numel * esz
+        self.raw = torch.full((nbytes + 2 * GUARD,), SENTINEL, dtype=torch.uint8, device=device)
+        self.tensor = self.raw[GUARD:GUARD + nbytes].view(dtype).view(shape)
+
+    def intact(self) -> bool:
+        torch.cuda.synchronize()
+        return bool((self.raw[:GUARD] == SENTINEL).all() and (self.raw[-GUARD:] == SENTINEL).all())
+
+
+def _maps(rng, n, p, q, normal=False):
+    a = rng.standard_normal((n, p, q)) if normal else rng.uniform(size=(n, p, q))
+    return a.astype(np.float32)
+
+
+@pytest.mark.parametrize("l,p,q,nm,tma", [(7, 40, 36, 2, True), (5, 28, 24, 3, True), (9, 33, 44, 1, True),
+                                          (7, 20, 21, 1, False), (3, 5, 6, 2, False), (7, 130, 128, 1, True)])
+def test_moments_repeatable_and_in_bounds(ex, l, p, q, nm, tma, monkeypatch):
+    if not tma:
+        monkeypatch.setenv("DDCCA_NO_TMA", "1")
+    rng = np.random.default_rng(l * 13 + q)
+    n, classes = 13, 4
+    m1 = torch.from_numpy(_maps(rng, n * nm, p, q)).to(ex.device)
+    m2 = torch.from_numpy(_maps(rng, n * nm, p, q, True)).to(ex.device)
+    lab = torch.from_numpy(np.repeat(np.arange(n) % classes, nm).astype(np.int32)).to(ex.device)
+    offs = np.array([0, 5 * nm, 9 * nm, n * nm], dtype=np.int64)
+    geom = P.PatchGeometry(l, l)
+    plen = E.payload_len(geom.dim, classes)
+    outs = []
+    for _ in range(4):
+        g = Guarded((3, plen), torch.float64, ex.device)
+        with torch.cuda.stream(ex.stream):
+            E.moments_partials(ex, m1, m2, lab, offs, geom, True, classes, out=g.tensor)
+        ex.synchronize()
+        assert g.intact()
+        outs.append(g.tensor.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("l,count,p,q,bh,bw,tc", [(7, 8, 128, 128, 16, 16, True), (5, 8, 112, 92, 7, 7, True),
+                                                  (3, 8, 40, 36, 8, 8, True), (7, 8, 64, 48, 16, 16, False),
+                                                  (9, 12, 40, 40, 8, 8, False), (5, 8, 28, 23, 7, 7, False)])
+def test_conv_hist_repeatable_and_in_bounds(ex, l, count, p, q, bh, bw, tc, monkeypatch):
+    """The tcgen05 kernel (TMEM, mbarrier rings, two MMA warps, two epilogue groups) and the FFMA
+    kernel: identical counts over repeated launches, persistent grids with more maps than CTAs."""
+    monkeypatch.setenv("DDCCA_CONV_TC", "1" if tc else "0")
+    rng = np.random.default_rng(l + q)
+    n_in = 8
+    maps = torch.from_numpy(_maps(rng, 40 * n_in, p, q, True)).to(ex.device)
+    f = rng.standard_normal((count, l, l))
+    plan = E.block_plan(P.EncoderConfig(bh, bw), p, q, count)
+    kind = E.count_kind(plan.bpc)
+    featlen = n_in * plan.blocks * plan.bins
+    lib = _native.load()
+    outs = []
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, P.PatchGeometry(l, l), True)
+    for _ in range(4):
+        g = Guarded((40, featlen), torch.int16 if kind == 2 else torch.uint8, ex.device)
+        g.tensor.zero_()
+        with torch.cuda.stream(ex.stream):
+            assert E.conv_hist(ex, maps, lay, 1, plan, g.tensor.view(-1), kind, n_in, featlen,
+                               plan.blocks * plan.bins, True)
+            path = lib.ddcca_conv_hist_last_path()
+        ex.synchronize()
+        assert g.intact()
+        outs.append(g.tensor.cpu().numpy())
+    assert path == (1 if tc else 0)  # the kernel under test really ran
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    assert E.decode_counts(outs[0], plan).reshape(40, -1, plan.bins).sum(axis=2).min() == plan.bpc
+
+
+@pytest.mark.parametrize("l,count,p,q", [(7, 8, 40, 36), (5, 8, 23, 30), (9, 12, 33, 41), (3, 8, 5, 6)])
+def test_conv_repeatable_and_in_bounds(ex, l, count, p, q):
+    rng = np.random.default_rng(l * 3 + q)
+    maps = torch.from_numpy(_maps(rng, 9, p, q)).to(ex.device)
+    f = rng.standard_normal((count, l, l))
+    outs = []
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, P.PatchGeometry(l, l), True)
+    for _ in range(3):
+        g = Guarded((9, count, p, q), torch.float32, ex.device)
+        with torch.cuda.stream(ex.stream):
+            E.conv(ex, maps, lay, 2, out=g.tensor)
+        ex.synchronize()
+        assert g.intact()
+        outs.append(g.tensor.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("d,classes,count", [(25, 40, 8), (49, 257, 8), (49, 8, 8), (81, 30, 12)])
+def test_solve_repeatable_and_in_bounds(ex, d, classes, count):
+    """finalize -> Newton-Schulz whitening -> DMMA Grams -> two parallel Jacobi CTAs -> filters."""
+    rng = np.random.default_rng(d + classes)
+    cols = 40 * classes
+    x, y = rng.standard_normal((d, cols)), rng.standard_normal((d, cols))
+    acc = P.MomentAccumulator.zeros(d, classes)
+    P.accumulate_batch(acc, x, y, np.arange(cols) % classes, ex)
+    payload = torch.from_numpy(acc.to_payload()).to(ex.device)
+    geom = P.PatchGeometry(int(np.sqrt(d)), int(np.sqrt(d)))
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(ex.stream):
+            lay = E.solve_layer(ex, payload, geom, count, True, classes, 1e-4)
+            outs.append((lay.w1.cpu().numpy(), lay.w2.cpu().numpy(), lay.pack1.cpu().numpy()))
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert np.array_equal(a, b)
+
+
+def test_nn_and_lut_repeatable(ex):
+    rng = np.random.default_rng(5)
+    tr = rng.standard_normal((300, 777))
+    q = rng.standard_normal((211, 777))
+    lab = np.arange(300) % 7
+    model = P.classify.fit(tr, lab, executor=ex)
+    first = P.classify.predict_many(model, q, executor=ex)
+    for _ in range(3):
+        assert np.array_equal(P.classify.predict_many(model, q, executor=ex), first)
