@@ -501,21 +501,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "note": "GEMM-equivalent bookkeeping: the exact FP64 lag form (85 DFMA per pixel at 7x7) does the "
                         "statistics a 3xTF32 Gram (2 d^2 = 4802 flop per patch) would; this is the Gram-convention "
                         "rate, the tensor pipe is idle in these kernels"}
-    if roof is not None:
-        # DRAM bytes per launch of the same kernel from the committed ncu launch list
-        tf = ROOT / "profiles" / "traffic.json"
-        kname = {"conv_hist": "conv_hist_kernel", "conv_l1": "conv_c_kernel", "conv_l2": "conv_c_kernel"}.get(
-            roof["kernel"], "lag_tma_kernel" if roof["kernel"].startswith("moments") else roof["kernel"])
-        if tf.exists():
-            t = json.loads(tf.read_text())
-            k = t.get("kernels", {}).get(kname) if t.get("workload", "caltech256") == args.workload else None
-            if k:
-                roof["traffic"] = k["dram_bytes_per_launch"]
-                roof["traffic_unit"] = "bytes/launch (dram read+write)"
-                roof["traffic_source"] = "profiles/traffic.json: " + t.get("source", "")
-                w = kern[roof["kernel"]]["work"] or {}
-                if w.get("bytes"):
-                    roof["algorithmic_bytes"] = w["bytes"]
+    # DRAM bytes per launch of the same kernels from the committed ncu launch list
+    tf = ROOT / "profiles" / "traffic.json"
+    tfd = json.loads(tf.read_text()) if tf.exists() else {}
+    for r in ([roof] if roof is not None else []) + list(rooflines.values()):
+        name = r["kernel"]
+        kname = {"conv_hist": "conv_hist_tc_kernel" if r.get("bound") == "tensor" else "conv_hist_kernel",
+                 "conv_l1": "conv_c_kernel", "conv_l2": "conv_c_kernel"}.get(
+            name, "lag_tma_kernel" if name.startswith("moments") else name)
+        k = tfd.get("kernels", {}).get(kname) if tfd.get("workload", "caltech256") == args.workload else None
+        if k:
+            r["traffic"] = k["dram_bytes_per_launch"]
+            r["traffic_unit"] = "bytes/launch (dram read+write)"
+            r["traffic_source"] = "profiles/traffic.json: " + tfd.get("source", "")
+            w = kern[name]["work"] or {}
+            if w.get("bytes"):
+                r["algorithmic_bytes"] = w["bytes"]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cpu_baseline(args.workload, args.cpu_sample)

@@ -2,7 +2,7 @@
 # Profile evidence for one round (run under gpurun from the repo root, ONE GPU):
 #   1) the bench command plain (must exit 0 before any ncu pass),
 #   2) its per-launch list (gpu__time_duration + DRAM bytes, --clock-control none),
-#   3) one full capture of each dominant kernel (fused conv-hist, lag moments, conv) and of the
+#   3) one full capture of each dominant kernel (tcgen05 conv-hist, lag moments, conv) and of the
 #      HBM-bound window sums (rect_sums).
 # Usage: tools/profile_round.sh [workload]   -> gpurun_out/prof_round/
 set -u
@@ -12,9 +12,9 @@ mkdir -p $OUT
 CMD="python bench.py --workload $WL --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 $CMD > $OUT/plain.json 2> $OUT/plain.err || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"ddcca|lag_|conv|solve|whiten|finalize|zone_reduce|assemble|rect_sums|batch_epilogue|tree_level|hist|sym_eig|iq_" \
+    -k regex:"ddcca|lag_|conv|solve|whiten|finalize|gram_kernel|eig2|finish|taps_prep|zone_reduce|assemble|rect_sums|batch_epilogue|tree_level|hist|sym_eig|iq_" \
     --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"conv_hist_kernel" -s 2 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:"conv_hist_tc_kernel" -s 2 -c 1 \
     -o $OUT/conv_hist $CMD > $OUT/ncu_full1.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:"lag_tma_kernel" -s 4 -c 1 \
     -o $OUT/lag_tma $CMD > $OUT/ncu_full2.log 2>&1
