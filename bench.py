@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--deterministic", type=int, default=1)
     ap.add_argument("--classify", action="store_true",
                     help="also run the device NN classifier on the step's counts (accuracy, fp64 GEMM rate)")
-    ap.add_argument("--moments", default="exact", choices=("exact", "blocked"),
+    ap.add_argument("--moments", default="blocked", choices=("exact", "blocked"),
                     help="lag-product precision of layers >= 2 (ExecSettings.moments)")
     return ap.parse_args()
 

@@ -1339,8 +1339,9 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
       if (ok) {
         const size_t max_stage =
             ((size_t)std::max(bx.rows_int * bx.mb_int, bx.rows_short * bx.mb_short) * tcb + 31) / 32 * 32;
-        bx.f64 = env_int("DDCCA_LAG_F32", 0) == 0 ? 1 : 0;
         bx.f32blocks = (flags & DDCCA_MOMENTS_F32_BLOCKS) ? 1 : 0;
+        // float64 compute tiles only for the exact form (the blocked form reads the float32 stages)
+        bx.f64 = (env_int("DDCCA_LAG_F32", 0) == 0 && !bx.f32blocks) ? 1 : 0;
         // float64 path: two compute tiles (one barrier per stage) and, by default, two float32
         // TMA stages, so two CTAs still fit one SM
         if (bx.f64 && !bx.f32blocks) bx.ns = std::max(2, std::min(8, env_int("DDCCA_TMA_STAGES", 2)));

@@ -11,6 +11,7 @@
 // CTA with the Jacobi matrices in shared memory is the right shape: the
 // solve is latency-bound (a few hundred rotation rounds), not FLOP-bound.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -125,6 +126,71 @@ __device__ __forceinline__ int lex_cmp(const double* v, int n, int ld, int i, in
   }
   return 0;
 }
+
+// Stable descending sort of eigenvalues wtmp (unsorted, final scale) with their eigenvector
+// columns va, the sign rule (solver.py:49-57) and the lexicographic order inside degenerate
+// runs (solver.py:60-79) -> w, v. tmp: n x n scratch. Shared by every eigensolver form.
+__device__ void eig_order(int n, double* wtmp, const double* va, double* w, double* v, double* tmp, Blk& B) {
+  const int nn = n * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int r = desc_rank(wtmp, n, i);
+    w[r] = wtmp[i];
+    for (int k = 0; k < n; ++k) tmp[k * n + r] = va[k * n + i];
+  }
+  __syncthreads();
+  // sign rule
+  col_signs(tmp, n, n, n, wtmp);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) tmp[e] *= wtmp[e % n];
+  __syncthreads();
+  // degenerate runs: |w[k] - w[start]| <= 1e-10 * max|w|, sorted lexicographically
+  int* run_start = B.iscr;  // n ints
+  if (threadIdx.x == 0) {
+    double sc = 0.0;
+    for (int i = 0; i < n; ++i) sc = fmax(sc, fabs(w[i]));
+    const double tol = 1e-10 * sc;
+    int start = 0;
+    for (int k = 1; k <= n; ++k) {
+      if (k < n && fabs(w[k] - w[start]) <= tol) continue;
+      for (int i = start; i < k; ++i) run_start[i] = start;
+      start = k;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int st = run_start[i];
+    int en = i + 1;
+    while (en < n && run_start[en] == st) ++en;
+    int r = st;
+    for (int j = st; j < en; ++j) {
+      if (j == i) continue;
+      const int c = lex_cmp(tmp, n, n, j, i);
+      if (c < 0 || (c == 0 && j < i)) ++r;
+    }
+    wtmp[r] = w[i];
+    for (int k = 0; k < n; ++k) v[k * n + r] = tmp[k * n + i];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = wtmp[i];
+  __syncthreads();
+}
+
+// C = op(A) * op(B) for n x n row-major matrices (ta/tb: use transpose)
+__device__ void matmul(const double* A, bool ta, const double* Bm, bool tb, double* C, int n, int kdim, int mcols) {
+  // C (n x mcols) = A' (n x kdim) * B' (kdim x mcols)
+  for (int e = threadIdx.x; e < n * mcols; e += blockDim.x) {
+    const int i = e / mcols, j = e - i * mcols;
+    double s = 0.0;
+    for (int k = 0; k < kdim; ++k) {
+      const double x = ta ? A[k * n + i] : A[i * kdim + k];
+      const double y = tb ? Bm[j * kdim + k] : Bm[k * mcols + j];
+      s += x * y;
+    }
+    C[e] = s;
+  }
+  __syncthreads();
+}
+
 
 // Symmetric eigensolver (solver.py:90-158). s: input n x n. Results: w (n),
 // v (n x n row-major, column j = eigenvector j). The rotation working set
@@ -278,69 +344,14 @@ __device__ int sym_eig_dev(const double* s, int n, double* w, double* v, double*
   PROF_MARK(t_post);
   // written as !(x <= tol) so a NaN off-diagonal norm is reported, never returned as converged
   if (!converged && !(offdiag_norm(a, n, B) <= 1e-12)) return DDCCA_ENUMERICAL;
-  // eigenvalues, stable descending order
+  // eigenvalues, stable descending order, sign rule, degenerate-run order
   for (int i = threadIdx.x; i < n; i += blockDim.x) wtmp[i] = a[i * n + i] * norm;
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int r = desc_rank(wtmp, n, i);
-    w[r] = wtmp[i];
-    for (int k = 0; k < n; ++k) tmp[k * n + r] = va[k * n + i];
-  }
-  __syncthreads();
-  // sign rule
-  col_signs(tmp, n, n, n, wtmp);
-  __syncthreads();
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) tmp[e] *= wtmp[e % n];
-  __syncthreads();
-  // degenerate runs: |w[k] - w[start]| <= 1e-10 * max|w|, sorted lexicographically
-  int* run_start = B.iscr;  // n ints
-  if (threadIdx.x == 0) {
-    double sc = 0.0;
-    for (int i = 0; i < n; ++i) sc = fmax(sc, fabs(w[i]));
-    const double tol = 1e-10 * sc;
-    int start = 0;
-    for (int k = 1; k <= n; ++k) {
-      if (k < n && fabs(w[k] - w[start]) <= tol) continue;
-      for (int i = start; i < k; ++i) run_start[i] = start;
-      start = k;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int st = run_start[i];
-    int en = i + 1;
-    while (en < n && run_start[en] == st) ++en;
-    int r = st;
-    for (int j = st; j < en; ++j) {
-      if (j == i) continue;
-      const int c = lex_cmp(tmp, n, n, j, i);
-      if (c < 0 || (c == 0 && j < i)) ++r;
-    }
-    wtmp[r] = w[i];
-    for (int k = 0; k < n; ++k) v[k * n + r] = tmp[k * n + i];
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = wtmp[i];
-  __syncthreads();
+  eig_order(n, wtmp, va, w, v, tmp, B);
   PROF_ADD(4, t_post);
   return DDCCA_OK;
 }
 
-// C = op(A) * op(B) for n x n row-major matrices (ta/tb: use transpose)
-__device__ void matmul(const double* A, bool ta, const double* Bm, bool tb, double* C, int n, int kdim, int mcols) {
-  // C (n x mcols) = A' (n x kdim) * B' (kdim x mcols)
-  for (int e = threadIdx.x; e < n * mcols; e += blockDim.x) {
-    const int i = e / mcols, j = e - i * mcols;
-    double s = 0.0;
-    for (int k = 0; k < kdim; ++k) {
-      const double x = ta ? A[k * n + i] : A[i * kdim + k];
-      const double y = tb ? Bm[j * kdim + k] : Bm[k * mcols + j];
-      s += x * y;
-    }
-    C[e] = s;
-  }
-  __syncthreads();
-}
 
 // C = A B for dp x dp row-major matrices in shared memory (dp % 8 == 0), on the FP64 tensor
 // path: one warp per 8 x 8 output tile, mma.sync m8n8k4 f64 over K (each product and sum in

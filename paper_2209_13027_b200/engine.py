@@ -473,7 +473,9 @@ class Engine:
             fl = 2.0 * 2 * nmaps * p * q * lags
             oh, ow = geom.out_shape(p, q)
             gfl = 2.0 * 2 * nmaps * oh * ow * geom.dim * geom.dim
-            self._timed(f"moments_l{len(layers) + 1}", 5, {"kind": "fp64", "flops": fl, "gram_flops": gfl,
+            # the blocked form (layers >= 2 by default) runs the lag products as FP32 FMAs
+            kind = "fma" if self.moments_flags(layers) & MOMENTS_F32_BLOCKS else "fp64"
+            self._timed(f"moments_l{len(layers) + 1}", 5, {"kind": kind, "flops": fl, "gram_flops": gfl,
                                                           "bytes": 8.0 * nmaps * p * q},
                         moments_partials, ex, m1, m2, mlab, offs, geom, center, classes,
                         out=parts[row:row + len(group)], flags=self.moments_flags(layers))
@@ -485,7 +487,7 @@ class Engine:
 
     def moments_flags(self, layers: list) -> int:
         """Float32-blocked lag products for layers fed by filter responses (ExecSettings.moments)."""
-        mode = getattr(self.ex.settings, "moments", "exact")
+        mode = getattr(self.ex.settings, "moments", "blocked")
         flags = MOMENTS_F32_BLOCKS if (layers and mode == "blocked") else 0
         if not layers:  # one map per sample: 32-map splits (4x the CTAs of the first layer)
             flags |= MOMENTS_FINE_SPLITS

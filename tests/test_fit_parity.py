@@ -58,7 +58,12 @@ POOL = O.Pool(threads=min(32, os.cpu_count() or 1))
 
 @pytest.fixture(scope="module")
 def ex():
-    return P.Executor(P.ExecSettings())
+    return P.Executor(P.ExecSettings())  # default: float32-blocked lag products on layers >= 2
+
+
+@pytest.fixture(scope="module")
+def ex_exact():
+    return P.Executor(P.ExecSettings(moments="exact"))
 
 
 def rel(a, b):
@@ -175,10 +180,13 @@ def _net(cfg, batch=128):
                            batch=P.BatchSpec(batch))
 
 
-def test_fit_parity_orl_full(ex):
-    """BASELINE c1 in full: 400 x 112x92, 40 classes, 8/8 filters 5x5 — every layer."""
+@pytest.mark.parametrize("mode", ["blocked", "exact"])
+def test_fit_parity_orl_full(ex, ex_exact, mode):
+    """BASELINE c1 in full: 400 x 112x92, 40 classes, 8/8 filters 5x5 — every layer, with the default
+    float32-blocked and the exact float64 lag products."""
     v1, v2, lab, cfg = synthetic.make_corpus("orl")
-    run_fit_parity(ex, v1.astype(np.float32), v2.astype(np.float32), lab, cfg["classes"], _net(cfg), 2)
+    run_fit_parity(ex if mode == "blocked" else ex_exact, v1.astype(np.float32), v2.astype(np.float32), lab,
+                   cfg["classes"], _net(cfg), 2)
 
 
 def test_fit_parity_caltech_subsample(ex):

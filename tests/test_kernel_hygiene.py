@@ -57,9 +57,10 @@ def _maps(rng, n, p, q, normal=False):
     return a.astype(np.float32)
 
 
+@pytest.mark.parametrize("blocked", [False, True])
 @pytest.mark.parametrize("l,p,q,nm,tma", [(7, 40, 36, 2, True), (5, 28, 24, 3, True), (9, 33, 44, 1, True),
                                           (7, 20, 21, 1, False), (3, 5, 6, 2, False), (7, 130, 128, 1, True)])
-def test_moments_repeatable_and_in_bounds(ex, l, p, q, nm, tma, monkeypatch):
+def test_moments_repeatable_and_in_bounds(ex, l, p, q, nm, tma, blocked, monkeypatch):
     if not tma:
         monkeypatch.setenv("DDCCA_NO_TMA", "1")
     rng = np.random.default_rng(l * 13 + q)
@@ -74,7 +75,8 @@ def test_moments_repeatable_and_in_bounds(ex, l, p, q, nm, tma, monkeypatch):
     for _ in range(4):
         g = Guarded((3, plen), torch.float64, ex.device)
         with torch.cuda.stream(ex.stream):
-            E.moments_partials(ex, m1, m2, lab, offs, geom, True, classes, out=g.tensor)
+            E.moments_partials(ex, m1, m2, lab, offs, geom, True, classes, out=g.tensor,
+                               flags=E.MOMENTS_F32_BLOCKS if blocked else 0)
         ex.synchronize()
         assert g.intact()
         outs.append(g.tensor.cpu().numpy())
