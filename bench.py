@@ -273,7 +273,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     bs = 128
     nb = -(-M // bs)
     mine = shard_range(nb, rank, world)
-    s0, s1 = mine.start * bs, min(M, mine.stop * bs)
+    s0, s1 = min(M, mine.start * bs), min(M, mine.stop * bs)  # a rank may own no batch (s0 == s1)
     ex = P.Executor(P.ExecSettings(deterministic=bool(args.deterministic), moments=args.moments), device=local_rank)
     layer_cfgs = [P.LayerConfig(L, P.PatchGeometry(l1, l2)) for L, l1, l2 in cfg["layers"]]
     enc = P.EncoderConfig(*cfg["block"])
@@ -281,7 +281,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # synthetic corpus for this rank's shard, generated on the device (not timed)
     with torch.cuda.stream(ex.stream):
         img1, lab = synthetic.blob_images_device(M, p, q, classes, seed=0, device=dev, start=s0, stop=s1)
-        img2 = synthetic.second_view_device(img1, cfg["view2"], seed=1)
+        img2 = synthetic.second_view_device(img1, cfg["view2"], seed=1, executor=ex)
         labels = torch.from_numpy(lab.astype(np.int32)).to(dev)
     ex.synchronize()
 
@@ -401,7 +401,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         h2 = img2.cpu().pin_memory()
         hl = torch.from_numpy(lab.astype(np.int64))
         host_counts = torch.empty((s1 - s0, featlen), dtype=torch.int16 if kind == 2 else torch.uint8).pin_memory()
-        ds = P.ViewPairDataset.from_arrays(h1, h2, hl.numpy(), class_count=classes)  # pinned: chunked async upload
+        # this rank's rows of the M-image dataset (pinned: chunked async upload)
+        ds = P.ViewPairDataset.shard(h1, h2, hl.numpy(), s0, M, classes)
         net = P.NetworkConfig(tuple(layer_cfgs), batch=P.BatchSpec(bs))
         pcfg = type("Cfg", (), {"net": net, "encoder": enc})()
 
@@ -434,10 +435,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         t = torch.tensor([ms_e], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        h2d = 2 * (s1 - s0) * p * q * 4 + (s1 - s0) * 8
-        d2h = host_counts.numel() * host_counts.element_size()
-        e2e = {"value": M / (float(t.item()) / 1000.0), "unit": "images/s", "h2d_bytes_per_step": h2d * world,
-               "d2h_bytes_per_step": d2h * world, "ms_per_step": float(t.item())}
+        # whole-job bytes per step (every rank copies its own shard's images in and counts out)
+        h2d = 2 * M * p * q * 4 + M * 8
+        d2h = M * featlen * host_counts.element_size()
+        e2e = {"value": M / (float(t.item()) / 1000.0), "unit": "images/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(t.item())}
 
     if rank != 0:
         return

@@ -230,19 +230,18 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
     import torch
 
     ex = _executor(executor)
-    v1, v2, lab = ds.stacks_view()
-    lab = np.asarray(lab)
-    if lab.size and (lab.min() < 0 or lab.max() >= ds.class_count):
-        raise ShapeError(f"label outside [0, {ds.class_count})")
-    n = len(lab)
+    n = ds.global_len
     bs = cfg.batch.batch_size
     gb = batch_partition(n, cfg.batch)
     mine = ex.shard(len(gb))
-    s0 = gb[mine.start].start if len(mine) else 0
-    s1 = gb[mine.stop - 1].stop if len(mine) else 0
+    s0 = gb[mine.start].start if len(mine) else ds.row_offset
+    s1 = gb[mine.stop - 1].stop if len(mine) else ds.row_offset
+    h1, h2, lab = ds.local_rows(s0, s1)
+    lab = np.asarray(lab)
+    if lab.size and (lab.min() < 0 or lab.max() >= ds.class_count):
+        raise ShapeError(f"label outside [0, {ds.class_count})")
     eng = E.Engine(ex)
     with torch.cuda.stream(ex.stream):
-        h1, h2 = _rows(v1, s0, s1), _rows(v2, s0, s1)
         if _pinned(h1) and _pinned(h2):
             # pinned host views: upload in chunks on a copy stream; the first layer's
             # moments start on each chunk as it lands (Engine.upload_events)
@@ -250,7 +249,7 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
         else:
             i1 = _to_dev32(ex, h1)
             i2 = _to_dev32(ex, h2)
-        ld = _labels_dev(ex, lab[s0:s1])
+        ld = _labels_dev(ex, lab)
         res = eng.fit(i1, i2, ld, ds.class_count, list(cfg.layers), bs, cfg.epsilon, n_global=n, first_sample=s0,
                       stage_hook=stage_hook)
         bank = _bank_from_device(res.layers)  # reads on the executor's stream

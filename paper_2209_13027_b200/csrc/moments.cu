@@ -256,39 +256,54 @@ __device__ __forceinline__ void lag_map(const S* __restrict__ t, int tc, int nro
 template <int L1, int TC, bool SKIP0, int KK>
 __device__ __forceinline__ void lag_accumulate_f32(const float* __restrict__ t, int nrows, int cown, int cpart,
                                                    double (&acc)[L1][KDX]) {
-  float fa[L1][KK];
+  // lags k = 0, 1 as packed fma.rn.f32x2 (the same per-lane rounding as two fmaf: bitwise the
+  // scalar form, half the issue slots), k = 2 scalar
+  constexpr bool P2 = KK >= 2;
+  constexpr bool S1 = KK != 2;  // a scalar lag: k = 2 of three, or the only one
+  constexpr int ks = P2 ? 2 : 0;
+  float2 fa2[L1];
+  float fa1[L1];
 #pragma unroll
-  for (int dy = 0; dy < L1; ++dy)
-#pragma unroll
-    for (int k = 0; k < KK; ++k) fa[dy][k] = 0.f;
-  float ring[L1][KK];
+  for (int dy = 0; dy < L1; ++dy) {
+    fa2[dy] = make_float2(0.f, 0.f);
+    fa1[dy] = 0.f;
+  }
+  float2 ring2[L1];
+  float ring1[L1];
   const float* pp = t + cpart;
 #pragma unroll
-  for (int q = 0; q < L1 - 1; ++q)
-#pragma unroll
-    for (int k = 0; k < KK; ++k) ring[q][k] = pp[q * TC + k];
+  for (int q = 0; q < L1 - 1; ++q) {
+    if constexpr (P2) ring2[q] = make_float2(pp[q * TC], pp[q * TC + 1]);
+    if constexpr (S1) ring1[q] = pp[q * TC + ks];
+  }
   pp += (L1 - 1) * TC;
   const float* po = t + cown;
   for (int r0 = 0; r0 < nrows; r0 += L1) {
 #pragma unroll
     for (int u = 0; u < L1; ++u) {
       const int snew = (u + L1 - 1) % L1;
-#pragma unroll
-      for (int k = 0; k < KK; ++k) ring[snew][k] = pp[u * TC + k];
+      if constexpr (P2) ring2[snew] = make_float2(pp[u * TC], pp[u * TC + 1]);
+      if constexpr (S1) ring1[snew] = pp[u * TC + ks];
       float own = po[u * TC];
       own = (r0 + u < nrows) ? own : 0.f;
+      const float2 own2 = make_float2(own, own);
 #pragma unroll
-      for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy)
-#pragma unroll
-        for (int k = 0; k < KK; ++k) fa[dy][k] = fmaf(own, ring[(u + dy) % L1][k], fa[dy][k]);
+      for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy) {
+        if constexpr (P2) fa2[dy] = __ffma2_rn(own2, ring2[(u + dy) % L1], fa2[dy]);
+        if constexpr (S1) fa1[dy] = fmaf(own, ring1[(u + dy) % L1], fa1[dy]);
+      }
     }
     pp += L1 * TC;
     po += L1 * TC;
   }
 #pragma unroll
-  for (int dy = 0; dy < L1; ++dy)
-#pragma unroll
-    for (int k = 0; k < KK; ++k) acc[dy][k] += (double)fa[dy][k];
+  for (int dy = 0; dy < L1; ++dy) {
+    if constexpr (P2) {
+      acc[dy][0] += (double)fa2[dy].x;
+      acc[dy][1] += (double)fa2[dy].y;
+    }
+    if constexpr (S1) acc[dy][ks] += (double)fa1[dy];
+  }
 }
 
 template <int L1, int TC>

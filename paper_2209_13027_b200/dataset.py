@@ -50,6 +50,36 @@ class ViewPairDataset:
     class_count: int
     label_map: dict = field(default_factory=dict)
     _stacks: tuple | None = field(default=None, repr=False)
+    # multi-GPU: the stacks hold rows [row_offset, row_offset + n) of a dataset of total_rows
+    # samples (ViewPairDataset.shard); train_network / compute_features only read their rank's rows
+    row_offset: int = 0
+    total_rows: int | None = None
+
+    @classmethod
+    def shard(cls, view1, view2, labels, first_row: int, total_rows: int, class_count: int, label_map=None):
+        """This rank's rows of a larger dataset (no host copy of the other ranks' samples): the fit and
+        the transform see a dataset of ``total_rows`` samples, batched and sharded as usual, and read
+        only rows [first_row, first_row + len(labels)), which must cover the rank's batch shard."""
+        ds = cls.from_arrays(view1, view2, labels, class_count=class_count, label_map=label_map)
+        if first_row < 0 or first_row + len(ds) > total_rows:
+            raise ShapeError(f"rows [{first_row}, {first_row + len(ds)}) outside a dataset of {total_rows}")
+        ds.row_offset = int(first_row)
+        ds.total_rows = int(total_rows)
+        return ds
+
+    @property
+    def global_len(self) -> int:
+        """Samples of the whole (possibly sharded) dataset."""
+        return self.total_rows if self.total_rows is not None else len(self)
+
+    def local_rows(self, s0: int, s1: int):
+        """(view1, view2, labels) rows [s0, s1) of the whole dataset, from this object's stacks."""
+        v1, v2, lab = self.stacks_view()
+        a, b = s0 - self.row_offset, s1 - self.row_offset
+        if a < 0 or b > len(lab):
+            raise ShapeError(f"rows [{s0}, {s1}) are not in this shard [{self.row_offset}, "
+                             f"{self.row_offset + len(lab)})")
+        return v1[a:b], v2[a:b], lab[a:b]
 
     @classmethod
     def from_arrays(cls, view1, view2, labels, class_count: int | None = None, label_map=None):

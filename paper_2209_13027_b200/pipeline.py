@@ -67,12 +67,11 @@ def compute_feature_counts(ds, bank, config, executor=None, host_out=None):
 
     ex = _executor(executor)
     enc, bs = _encoder_and_batch(config)
-    v1, v2, _ = ds.stacks_view()
-    n = len(ds)
+    n = ds.global_len
     gb = batch_partition(n, config.net.batch) if hasattr(config, "net") else [range(0, n)]
     mine = ex.shard(len(gb))
-    s0 = gb[mine.start].start if len(mine) else 0
-    s1 = gb[mine.stop - 1].stop if len(mine) else 0
+    s0 = gb[mine.start].start if len(mine) else ds.row_offset
+    s1 = gb[mine.stop - 1].stop if len(mine) else ds.row_offset
     st = getattr(ds, "_device_state", None)
     with torch.cuda.stream(ex.stream):
         layers = device_layers(bank, ex)
@@ -81,8 +80,9 @@ def compute_feature_counts(ds, bank, config, executor=None, host_out=None):
             i1, i2 = st["images"]
         else:
             eng = E.Engine(ex)
-            i1 = _to_dev32(ex, v1[s0:s1])
-            i2 = _to_dev32(ex, v2[s0:s1])
+            r1, r2, _ = ds.local_rows(s0, s1)
+            i1 = _to_dev32(ex, r1)
+            i2 = _to_dev32(ex, r2)
         counts, plan = eng.transform_counts(i1, i2, layers, enc, bs, host_out=host_out)
     handoff(ex, counts)
     if host_out is not None and eng.host_copy_done is not None:
@@ -115,7 +115,7 @@ def feature_rows(ds, config, executor=None) -> range:
     from .patches import batch_partition
 
     ex = _executor(executor)
-    n = len(ds)
+    n = ds.global_len
     gb = batch_partition(n, config.net.batch) if hasattr(config, "net") else [range(0, n)]
     mine = ex.shard(len(gb))
     if not len(mine):

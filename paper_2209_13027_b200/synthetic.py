@@ -108,14 +108,16 @@ def blob_images_device(n: int, p: int, q: int, classes: int, seed: int = 0, nois
     return out, labels[start:stop].astype(np.int64)
 
 
-def second_view_device(view1, kind: str, seed: int = 1, noise: float = 0.02):
+def second_view_device(view1, kind: str, seed: int = 1, noise: float = 0.02, executor=None):
     """Torch version of second_view for 'pair' and 'lbp' (device tensors)."""
     import torch
 
     if kind == "lbp":
+        from .execution import Executor
         from .views import lbp_stack
 
-        return lbp_stack(view1)  # the ddcca_lbp kernel (views.py:41-58)
+        ex = executor if executor is not None else Executor(device=view1.device)
+        return lbp_stack(view1, ex)  # the ddcca_lbp kernel (views.py:41-58), on view1's device
     if kind in ("pair", "channel"):
         sm = view1.clone()
         sm[:, 1:-1, 1:-1] = (view1[:, :-2, 1:-1] + view1[:, 2:, 1:-1] + view1[:, 1:-1, :-2] + view1[:, 1:-1, 2:]
