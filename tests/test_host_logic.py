@@ -112,3 +112,23 @@ def test_payload_length_law():
     # [c11 | c22 | s1 | s2 | g1 | g2 | n | n_c]
     for d, c in ((25, 40), (49, 8), (49, 257), (81, 257)):
         assert E.payload_len(d, c) == 2 * d * d + 2 * d * c + 2 * d + 1 + c
+
+
+def test_sharded_dataset_rows():
+    """ViewPairDataset.shard: a rank's rows of a larger dataset (multi-GPU e2e inputs)."""
+    import numpy as np
+    import pytest
+
+    import paper_2209_13027_b200 as P
+
+    v = np.arange(5 * 3 * 2, dtype=np.float32).reshape(5, 3, 2)
+    ds = P.ViewPairDataset.shard(v, v + 1, np.array([0, 1, 2, 0, 1]), 10, 20, 3)
+    assert len(ds) == 5 and ds.global_len == 20 and ds.row_offset == 10
+    a, b, lab = ds.local_rows(11, 14)
+    assert np.array_equal(a, v[1:4]) and np.array_equal(b, v[1:4] + 1) and lab.tolist() == [1, 2, 0]
+    with pytest.raises(P.ShapeError):
+        ds.local_rows(9, 12)
+    with pytest.raises(P.ShapeError):
+        P.ViewPairDataset.shard(v, v, np.zeros(5, int), 18, 20, 3)
+    full = P.ViewPairDataset.from_arrays(v, v, np.zeros(5, int))
+    assert full.global_len == 5 and full.local_rows(0, 5)[0].shape == (5, 3, 2)
