@@ -457,14 +457,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         r = {"kernel": name, "share_of_step": k["ms_per_step"] / ms, "ms_per_launch": k["ms_avg"]}
         if w.get("kind") == "tensor":
             # algorithmic flops = the convolution's own 2 * taps * filters per pixel (single pass);
-            # executed = what the tensor pipe ran (3xTF32 split products, banded B of K = 16 per tap row)
+            # executed = what the tensor pipe ran (two-term f16 split: 3 MMAs per product, banded B of
+            # K = 16 per tap row). peak = the measured dense bf16 rate (MEASURED_PEAKS.json; kind::f16
+            # runs at the bf16 rate); f16_mma_tflops = the tcgen05 f16 rate at this clock (2x the
+            # measured TF32 MMA rate: a K16 f16 MMA takes the cycles of a K8 tf32 one, f16_probe.cu)
             ex_tf = w.get("tensor_flops", 0.0) / t / 1e12
-            r.update({"bound": "tensor", "achieved": ach, "peak": cp["tf32_tflops"], "unit": "TFLOP/s",
-                      "frac": ach / cp["tf32_tflops"], "executed_tflops": ex_tf,
-                      "tensor_pipe_frac": ex_tf / cp["tf32_tflops"], "vs_ffma_peak": ach / cp["ffma_tflops"],
-                      "note": "tcgen05 kind::tf32, 3xTF32 (3 MMAs per product) x banded B (16 K columns per "
-                              "7 taps): executed = 6.9x algorithmic at 7x7; vs_ffma_peak = algorithmic rate over "
-                              "the FP32 CUDA-core peak the FFMA kernel is capped by"})
+            f16 = 2.0 * cp["tf32_tflops"]
+            r.update({"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                      "frac": ach / pk["bf16_tflops"], "executed_tflops": ex_tf, "f16_mma_tflops": f16,
+                      "tensor_pipe_frac": ex_tf / f16, "vs_ffma_peak": ach / cp["ffma_tflops"],
+                      "note": "tcgen05 kind::f16, power-of-two scaled two-term split (3 MMAs per product) x "
+                              "banded B (16 K columns per 7 taps): executed = 6.9x algorithmic at 7x7; "
+                              "tensor_pipe_frac = executed over the f16 MMA rate; vs_ffma_peak = algorithmic "
+                              "rate over the FP32 CUDA-core peak the FFMA kernel is capped by"})
         elif w.get("kind") == "fma":
             r.update({"bound": "fp32_fma", "achieved": ach, "peak": cp["ffma_tflops"], "unit": "TFLOP/s",
                       "frac": ach / cp["ffma_tflops"]})

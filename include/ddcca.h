@@ -187,8 +187,9 @@ DDCCA_API int ddcca_conv_hash(const float* in, int64_t n_maps, const ddcca_geom*
  * no host round trip between the solve and the next layer's conv). The bank
  * is one per device: calls on different streams of one device must be
  * ordered by the caller. ddcca_conv_hist_* runs on the tcgen05 tensor cores
- * (3xTF32) when the inputs need no DC shift and the shape is covered (maps of
- * <= 128 rows, q % 4 == 0, <= 8 filters, 3/5/7 windows; DDCCA_CONV_TC=0
+ * (kind::f16, maps and filters scaled by powers of two and split into f16 hi + lo:
+ * float32-level responses) when the inputs need no DC shift and the shape is covered
+ * (maps of <= 128 rows, q % 4 == 0, <= 8 filters, 3/5/7 windows; DDCCA_CONV_TC=0
  * forces the FFMA kernel). DDCCA_ECONFIG means "shape not covered" (use ddcca_conv /
  * ddcca_conv_hash + ddcca_block_hist). ddcca_conv_hist_hw fuses the last
  * layer's conv, sign hash and non-overlapping block histograms (K6-final +
@@ -204,7 +205,7 @@ DDCCA_API int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_ge
                                  int count, int center, int block_h, int block_w, void* counts, int count_kind,
                                  int64_t groups_per_row, int64_t row_stride, int64_t group_stride, void* stream);
 /* Which kernel the calling thread's last ddcca_conv_hist_* call launched: 1 = tcgen05 tensor
- * cores (3xTF32), 0 = FFMA. For roofline accounting. */
+ * cores (f16 two-term split), 0 = FFMA. For roofline accounting. */
 DDCCA_API int ddcca_conv_hist_last_path(void);
 DDCCA_API int ddcca_conv_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,
                              int count, int center, float* out, void* stream);

@@ -1,4 +1,4 @@
-// Tensor-core (tcgen05, 3xTF32) fused last-layer conv + sign hash + block histograms.
+// Tensor-core (tcgen05 kind::f16, scaled two-term split) fused last-layer conv + sign hash + block histograms.
 #pragma once
 #include <cuda_runtime.h>
 

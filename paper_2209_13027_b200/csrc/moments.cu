@@ -250,24 +250,24 @@ __device__ __forceinline__ void lag_map(const S* __restrict__ t, int tc, int nro
 }
 
 // Blocked float32 form (layers whose inputs are filter responses): the products of one
-// map's rows accumulate in float32 (at most one slab, <= SLAB_ROWS terms per lag) and
-// the per-map partial is added to the float64 accumulator. Used only when the caller
+// stage's maps accumulate in float32 (at most mb maps of one slab: <= STAGE_ROWS terms per
+// lag) and the stage partial is added to the float64 accumulator. Used only when the caller
 // asks for it (DDCCA_MOMENTS_F32_BLOCKS); float64 products are exact, these are not.
+// Lags k = 0, 1 run as packed fma.rn.f32x2 (the same per-lane rounding as two fmaf, half the
+// issue slots), k = 2 scalar; fa2 holds lags (0, 1), fa1 the scalar lag (k = 2 of three,
+// or k = 0 when the group has a single live lag).
+template <int L1>
+struct F32Partials {
+  float2 fa2[L1];
+  float fa1[L1];
+};
+
 template <int L1, int TC, bool SKIP0, int KK>
 __device__ __forceinline__ void lag_accumulate_f32(const float* __restrict__ t, int nrows, int cown, int cpart,
-                                                   double (&acc)[L1][KDX]) {
-  // lags k = 0, 1 as packed fma.rn.f32x2 (the same per-lane rounding as two fmaf: bitwise the
-  // scalar form, half the issue slots), k = 2 scalar
+                                                   F32Partials<L1>& f) {
   constexpr bool P2 = KK >= 2;
   constexpr bool S1 = KK != 2;  // a scalar lag: k = 2 of three, or the only one
   constexpr int ks = P2 ? 2 : 0;
-  float2 fa2[L1];
-  float fa1[L1];
-#pragma unroll
-  for (int dy = 0; dy < L1; ++dy) {
-    fa2[dy] = make_float2(0.f, 0.f);
-    fa1[dy] = 0.f;
-  }
   float2 ring2[L1];
   float ring1[L1];
   const float* pp = t + cpart;
@@ -289,38 +289,76 @@ __device__ __forceinline__ void lag_accumulate_f32(const float* __restrict__ t, 
       const float2 own2 = make_float2(own, own);
 #pragma unroll
       for (int dy = SKIP0 ? 1 : 0; dy < L1; ++dy) {
-        if constexpr (P2) fa2[dy] = __ffma2_rn(own2, ring2[(u + dy) % L1], fa2[dy]);
-        if constexpr (S1) fa1[dy] = fmaf(own, ring1[(u + dy) % L1], fa1[dy]);
+        if constexpr (P2) f.fa2[dy] = __ffma2_rn(own2, ring2[(u + dy) % L1], f.fa2[dy]);
+        if constexpr (S1) f.fa1[dy] = fmaf(own, ring1[(u + dy) % L1], f.fa1[dy]);
       }
     }
     pp += L1 * TC;
     po += L1 * TC;
   }
+}
+
+// Short tasks (single border rows) in the blocked form: direct partner loads.
+template <int L1, int TC, int KK>
+__device__ __forceinline__ void lag_accumulate_short_f32(const float* __restrict__ t, int nrows, int cown,
+                                                         int cpart, bool skip0, F32Partials<L1>& f) {
+  constexpr bool P2 = KK >= 2;
+  constexpr bool S1 = KK != 2;
+  constexpr int ks = P2 ? 2 : 0;
+  for (int r = 0; r < nrows; ++r) {
+    const float own = t[r * TC + cown];
+    const float2 own2 = make_float2(own, own);
+    const float* pp = t + r * TC + cpart;
+#pragma unroll
+    for (int dy = 0; dy < L1; ++dy) {
+      if (dy == 0 && skip0) continue;
+      if constexpr (P2) f.fa2[dy] = __ffma2_rn(own2, make_float2(pp[dy * TC], pp[dy * TC + 1]), f.fa2[dy]);
+      if constexpr (S1) f.fa1[dy] = fmaf(own, pp[dy * TC + ks], f.fa1[dy]);
+    }
+  }
+}
+
+template <int L1>
+__device__ __forceinline__ void f32_zero(F32Partials<L1>& f) {
 #pragma unroll
   for (int dy = 0; dy < L1; ++dy) {
-    if constexpr (P2) {
-      acc[dy][0] += (double)fa2[dy].x;
-      acc[dy][1] += (double)fa2[dy].y;
-    }
-    if constexpr (S1) acc[dy][ks] += (double)fa1[dy];
+    f.fa2[dy] = make_float2(0.f, 0.f);
+    f.fa1[dy] = 0.f;
   }
+}
+
+// Add the float32 stage partials to the float64 accumulator (and restart them).
+template <int L1>
+__device__ __forceinline__ void f32_flush(F32Partials<L1>& f, int kk, double (&acc)[L1][KDX]) {
+  // static lag indices on every branch: a runtime index into acc would move it to local memory
+#pragma unroll
+  for (int dy = 0; dy < L1; ++dy) {
+    if (kk >= 2) {
+      acc[dy][0] += (double)f.fa2[dy].x;
+      acc[dy][1] += (double)f.fa2[dy].y;
+      if (kk >= 3) acc[dy][2] += (double)f.fa1[dy];
+    } else {
+      acc[dy][0] += (double)f.fa1[dy];
+    }
+  }
+  f32_zero(f);
 }
 
 template <int L1, int TC>
 __device__ __forceinline__ void lag_map_f32(const float* __restrict__ t, int nrows, int cown, int cpart,
-                                            bool short_task, bool skip0, int kk, double (&acc)[L1][KDX]) {
-  if (short_task) {  // single border rows: few products, keep them exact
-    if (kk >= 3) lag_accumulate_short<L1, TC, 3>(t, TC, nrows, cown, cpart, skip0, acc);
-    else if (kk == 2) lag_accumulate_short<L1, TC, 2>(t, TC, nrows, cown, cpart, skip0, acc);
-    else lag_accumulate_short<L1, TC, 1>(t, TC, nrows, cown, cpart, skip0, acc);
+                                            bool short_task, bool skip0, int kk, F32Partials<L1>& f) {
+  if (short_task) {
+    if (kk >= 3) lag_accumulate_short_f32<L1, TC, 3>(t, nrows, cown, cpart, skip0, f);
+    else if (kk == 2) lag_accumulate_short_f32<L1, TC, 2>(t, nrows, cown, cpart, skip0, f);
+    else lag_accumulate_short_f32<L1, TC, 1>(t, nrows, cown, cpart, skip0, f);
   } else if (skip0) {
-    lag_accumulate_f32<L1, TC, true, 3>(t, nrows, cown, cpart, acc);
+    lag_accumulate_f32<L1, TC, true, 3>(t, nrows, cown, cpart, f);
   } else if (kk >= 3) {
-    lag_accumulate_f32<L1, TC, false, 3>(t, nrows, cown, cpart, acc);
+    lag_accumulate_f32<L1, TC, false, 3>(t, nrows, cown, cpart, f);
   } else if (kk == 2) {
-    lag_accumulate_f32<L1, TC, false, 2>(t, nrows, cown, cpart, acc);
+    lag_accumulate_f32<L1, TC, false, 2>(t, nrows, cown, cpart, f);
   } else {
-    lag_accumulate_f32<L1, TC, false, 1>(t, nrows, cown, cpart, acc);
+    lag_accumulate_f32<L1, TC, false, 1>(t, nrows, cown, cpart, f);
   }
 }
 
@@ -560,6 +598,8 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
     const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
     const int kk = min(KDX, 2 * A.l2 - 1 - grp * KDX);  // live lags of this group
     if (bx.f32blocks) {
+      F32Partials<L1> fp;
+      f32_zero(fp);
       for (int s = 0; s < nstages; ++s) {
         const int slot = s % NS;
         mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
@@ -567,9 +607,10 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
         const int64_t ms = ma + (int64_t)s * mb;
         const int nm = (int)min((int64_t)mb, mbnd - ms);
         for (int j = 0; j < nm; ++j)
-          lag_map_f32<L1, TCB>(tile + j * tile_elems, nrows, cown, cpart, short_task, skip0, kk, acc);
+          lag_map_f32<L1, TCB>(tile + j * tile_elems, nrows, cown, cpart, short_task, skip0, kk, fp);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
+        f32_flush(fp, kk, acc);  // one float64 flush per stage of mb maps
       }
     } else if (bx.f64) {
       // convert each landed float32 stage once into a float64 tile shared by all consumer

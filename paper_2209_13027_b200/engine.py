@@ -618,11 +618,11 @@ class Engine:
                     if self._timed("conv_hist", 1, wk, conv_hist, ex, maps, last, view, plan, base, kind, groups,
                                    featlen, plan.blocks * plan.bins, len(layers) > 1):
                         if lib.ddcca_conv_hist_last_path() == 1 and self.profile is not None:
-                            # tcgen05 3xTF32 kernel (convtc.cu): 3 MMAs M128 x N(8 filters x 8 columns) x K8
-                            # per tap row and 8-column K chunk, 2 chunks per 8 output columns, 128-row tiles
+                            # tcgen05 f16 kernel (convtc.cu): 3 MMAs M128 x N(8 filters x 8 columns) x K16
+                            # per tap row and 8-output-column block, 128-row tiles
                             blocks = -(-nb_cols // 8)
                             tiles = -(-pp // 128)
-                            ex_fl = 2.0 * 128 * 64 * 8 * 3 * 2 * last.geom.l1 * blocks * tiles * n
+                            ex_fl = 2.0 * 128 * 64 * 16 * 3 * last.geom.l1 * blocks * tiles * n
                             acc = self.work["conv_hist"]
                             acc["kind"] = "tensor"
                             acc["tensor_flops"] = acc.get("tensor_flops", 0.0) + ex_fl
