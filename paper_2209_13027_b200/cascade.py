@@ -244,12 +244,13 @@ def train_network(ds, cfg: NetworkConfig, executor, stage_hook=None) -> FilterBa
     with torch.cuda.stream(ex.stream):
         if _pinned(h1) and _pinned(h2):
             # pinned host views: upload in chunks on a copy stream; the first layer's
-            # moments start on each chunk as it lands (Engine.upload_events)
-            i1, i2, eng.upload_events = _upload_chunked(ex, h1, h2, UPLOAD_CHUNK_BATCHES * bs)
+            # moments start on each chunk as it lands (Engine.uploader)
+            eng.uploader = ChunkedUpload(ex, h1, h2, lab, UPLOAD_CHUNK_BATCHES * bs)
+            i1, i2, ld = eng.uploader.d1, eng.uploader.d2, eng.uploader.labels
         else:
             i1 = _to_dev32(ex, h1)
             i2 = _to_dev32(ex, h2)
-        ld = _labels_dev(ex, lab)
+            ld = _labels_dev(ex, lab)
         res = eng.fit(i1, i2, ld, ds.class_count, list(cfg.layers), bs, cfg.epsilon, n_global=n, first_sample=s0,
                       stage_hook=stage_hook)
         bank = _bank_from_device(res.layers)  # reads on the executor's stream
@@ -270,37 +271,70 @@ def _pinned(a) -> bool:
     return isinstance(a, torch.Tensor) and a.dtype == torch.float32 and a.is_pinned() and a.is_contiguous()
 
 
-def _upload_chunked(ex, h1, h2, rows_per_chunk: int):
-    """Pinned (m, p, q) float32 views -> device tensors filled chunk by chunk on a side stream.
+class ChunkedUpload:
+    """Pinned (m, p, q) float32 views (+ labels) -> device tensors, chunk by chunk on the
+    executor's persistent upload stream, submitted lazily.
 
-    Returns (d1, d2, [(row_end, event)]); ex.stream must wait on a chunk's event
-    before reading its rows (Engine.layer_partials does).
+    A chunk's copies are enqueued only when the fit reaches rows ``lookahead`` chunks before
+    it (``event_for``): host->device copies share the copy engine in submission order, so
+    submitting the whole image upload up front would queue every small copy the fit issues
+    on the compute stream (plan tables, label slices) behind all of it -- the first layer's
+    moments could then not start before the last chunk landed. The labels go first (pinned,
+    asynchronous) and the compute stream waits for them.
     """
-    import torch
 
-    m = h1.shape[0]
-    up = getattr(ex, "upload_stream", None)
-    if up is None:
-        up = ex.upload_stream = torch.cuda.Stream(device=ex.device)
-    # Buffers are allocated on the executor's persistent upload stream and marked as used by
-    # the compute stream: the caching allocator then never hands this step's upload a block
-    # that earlier compute work may still read, so the upload need not wait for the compute
-    # stream -- the next fit's images stream in while the previous transform still runs.
-    with torch.cuda.stream(up):
-        d1 = torch.empty(h1.shape, dtype=torch.float32, device=ex.device)
-        d2 = torch.empty(h2.shape, dtype=torch.float32, device=ex.device)
-    events = []
-    with torch.cuda.stream(up):
-        for r0 in range(0, m, max(1, rows_per_chunk)):
-            r1 = min(m, r0 + rows_per_chunk)
-            d1[r0:r1].copy_(h1[r0:r1], non_blocking=True)
-            d2[r0:r1].copy_(h2[r0:r1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(up)
-            events.append((r1, ev))
-    d1.record_stream(ex.stream)
-    d2.record_stream(ex.stream)
-    return d1, d2, events
+    def __init__(self, ex, h1, h2, labels, rows_per_chunk: int, lookahead: int = 2):
+        import torch
+
+        m = h1.shape[0]
+        up = getattr(ex, "upload_stream", None)
+        if up is None:
+            up = ex.upload_stream = torch.cuda.Stream(device=ex.device)
+        self.ex, self.up, self.h1, self.h2 = ex, up, h1, h2
+        self.lookahead = max(0, int(lookahead))
+        step = max(1, rows_per_chunk)
+        self.ends = [min(m, r0 + step) for r0 in range(0, m, step)]
+        self.events = []
+        # Buffers are allocated on the upload stream and marked as used by the compute stream:
+        # the caching allocator then never hands this upload a block that earlier compute work
+        # may still read, so the upload need not wait for the compute stream -- the next fit's
+        # images stream in while the previous transform still runs.
+        self._lab_host = torch.from_numpy(np.ascontiguousarray(np.asarray(labels, dtype=np.int32))).pin_memory()
+        with torch.cuda.stream(up):
+            self.d1 = torch.empty(h1.shape, dtype=torch.float32, device=ex.device)
+            self.d2 = torch.empty(h2.shape, dtype=torch.float32, device=ex.device)
+            self.labels = self._lab_host.to(ex.device, non_blocking=True)
+            lab_ev = torch.cuda.Event()
+            lab_ev.record(up)
+        for t in (self.d1, self.d2, self.labels):
+            t.record_stream(ex.stream)
+        ex.stream.wait_event(lab_ev)
+
+    def _submit(self, upto: int):
+        import torch
+
+        upto = min(upto, len(self.ends) - 1)
+        with torch.cuda.stream(self.up):
+            while len(self.events) <= upto:
+                i = len(self.events)
+                r0 = self.ends[i - 1] if i else 0
+                r1 = self.ends[i]
+                self.d1[r0:r1].copy_(self.h1[r0:r1], non_blocking=True)
+                self.d2[r0:r1].copy_(self.h2[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.up)
+                self.events.append(ev)
+
+    def event_for(self, row_end: int):
+        """Event after which rows [0, row_end) are on the device (submits chunks as needed)."""
+        i = next((k for k, e in enumerate(self.ends) if e >= row_end), len(self.ends) - 1)
+        self._submit(i + self.lookahead)
+        return self.events[i]
+
+    def finish(self):
+        """Submit every remaining chunk; the event of the last one."""
+        self._submit(len(self.ends) - 1)
+        return self.events[-1] if self.events else None
 
 
 def _rows(a, s0: int, s1: int):

@@ -324,7 +324,7 @@ class Engine:
     def __init__(self, executor, map_budget_bytes: int = MAP_BUDGET_BYTES, keep_maps_bytes: int = KEEP_MAPS_BYTES):
         self.ex = executor
         self.budget = map_budget_bytes
-        self.upload_events = []  # [(local row end, cuda event)] of an in-flight chunked image upload
+        self.uploader = None  # cascade.ChunkedUpload of an in-flight chunked image upload
         self.keep_maps_bytes = keep_maps_bytes
         self.maps_cache = None  # last hidden layer's maps of the fitted shard, reused by the transform
         self.profile = None   # dict name -> [(start_event, end_event)] when profiling
@@ -446,18 +446,15 @@ class Engine:
                         torch.empty((m_local * n_in, p, q), dtype=torch.float32, device=ex.device))
         row = 0
         groups = self._superbatches(batch_ranges, n_in * p * q * 4)
-        uploads = self.upload_events if not layers else []
-        if uploads:
+        up = self.uploader if not layers else None
+        if up is not None:
             # images still arriving (train_network's chunked upload): one group per upload
             # chunk, each waiting only for its own rows, so the copies overlap the moments
-            ends = [e for e, _ in uploads]
-            groups = self._split_at(groups, ends, first_sample)
+            groups = self._split_at(groups, up.ends, first_sample)
         for group in groups:
             s0, s1 = group[0].start - first_sample, group[-1].stop - first_sample
-            for end, ev in uploads:
-                if end >= s1:
-                    ex.stream.wait_event(ev)
-                    break
+            if up is not None:
+                ex.stream.wait_event(up.event_for(s1))
             if keep_buf is not None:
                 m1 = self._forward(images1[s0:s1], layers, 1, out=keep_buf[0][s0 * n_in:s1 * n_in])
                 m2 = self._forward(images2[s0:s1], layers, 2, out=keep_buf[1][s0 * n_in:s1 * n_in])
@@ -547,7 +544,11 @@ class Engine:
                 if keep_stats:
                     stats.append(merged)
             check_layers(layers)
-        self.upload_events = []
+        if self.uploader is not None:
+            ev = self.uploader.finish()  # (every chunk was reached by the first layer)
+            if ev is not None:
+                ex.stream.wait_event(ev)
+            self.uploader = None
         return FitResult(layers, stats)
 
     # -- transform ---------------------------------------------------------
