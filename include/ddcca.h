@@ -207,6 +207,11 @@ DDCCA_API int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_ge
 /* Which kernel the calling thread's last ddcca_conv_hist_* call launched: 1 = tcgen05 tensor
  * cores (f16 two-term split), 0 = FFMA. For roofline accounting. */
 DDCCA_API int ddcca_conv_hist_last_path(void);
+/* Which kernel the calling thread's last ddcca_conv_hw / ddcca_conv_dev call launched: 1 =
+ * tcgen05 tensor cores (same kind::f16 split as the conv-histogram, each map shifted by its mean
+ * for centered windows; "same" padding, l1 == l2 in {3, 5, 7}, <= 8 filters, maps of <= 128
+ * rows, q % 4 == 0), 0 = FFMA constant-bank kernel. For roofline accounting. */
+DDCCA_API int ddcca_conv_last_path(void);
 DDCCA_API int ddcca_conv_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,
                              int count, int center, float* out, void* stream);
 DDCCA_API int ddcca_conv_hist_dev(const float* in, int64_t n_maps, const ddcca_geom* g, const float* conv_pack,

@@ -56,6 +56,7 @@ _SIGNATURES = {
     "ddcca_conv_hist_hw": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp]),
     "ddcca_conv_dev": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _vp, _vp]),
     "ddcca_conv_hist_last_path": (_i32, []),
+    "ddcca_conv_last_path": (_i32, []),
     "ddcca_conv_hist_dev": (_i32, [_vp, _i64, _GP, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i64, _i64, _i64, _vp]),
     "ddcca_nn_workspace": (_sz, [_i64, _i64]),
     "ddcca_nn_classify": (_i32, [_vp, _i64, _vp, _i64, _i64, _i32, _vp, _i32, _vp, _i32, _vp, _vp, _sz, _vp]),

@@ -589,6 +589,7 @@ using namespace ddcca;
 namespace {
 
 thread_local int g_last_hist_path = 0;  // 1: the last conv-histogram launch ran on the tensor cores
+thread_local int g_last_conv_path = 0;  // 1: the last conv (responses) launch ran on the tensor cores
 
 int conv_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* pack, bool pack_dev, int count,
                int center, float* out, void* stream) {
@@ -598,10 +599,30 @@ int conv_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const floa
   if (count < 1 || count > g.d) return fail(DDCCA_ECONFIG, "filter count %d outside [1, %d]", count, g.d);
   if (!pack) return fail(DDCCA_ESHAPE, "null taps");
   if (n_maps == 0) return DDCCA_OK;
+  cudaStream_t st = as_stream(stream);
+  g_last_conv_path = 0;
+  if (g.l1 == g.l2 && g.oh == g.p && g.ow == g.q) {
+    // tensor-core kernel (convtc.cu, responses mode): each map shifted by its mean when the
+    // windows are centered (zero-mean taps: the responses do not depend on the shift)
+    TcHistArgs t{};
+    t.in = in; t.n_maps = n_maps; t.p = g.p; t.q = g.q; t.top = g.top; t.left = g.left; t.l = g.l1;
+    t.count = count; t.center = center & 1; t.resp = out; t.dc_shift = center & 1; t.nbits = 1;
+    if (conv_resp_tc_covers(t)) {
+      float* stage = nullptr;
+      if (cudaGetSymbolAddress(reinterpret_cast<void**>(&stage), g_taps_stage) != cudaSuccess)
+        return fail(DDCCA_ECUDA, "tap stage symbol");
+      DDCCA_TRY(stage_taps(pack, pack_dev, count, g.d, TC_FILTERS, center & 1, false, st));
+      const int rc = conv_resp_tc(t, stage, st);
+      if (rc != DDCCA_ECONFIG) {
+        g_last_conv_path = rc == DDCCA_OK ? 1 : 0;
+        return rc;
+      }
+    }
+  }
   CArgs A{};
   A.in = in; A.n_maps = n_maps; A.p = g.p; A.q = g.q; A.top = g.top; A.left = g.left; A.oh = g.oh; A.ow = g.ow;
   A.count = count; A.center = center; A.out = out;
-  return dispatch<false>(A, g.l1, g.l2, pack, pack_dev, as_stream(stream));
+  return dispatch<false>(A, g.l1, g.l2, pack, pack_dev, st);
 }
 
 int conv_hist_entry(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* pack, bool pack_dev,
@@ -670,6 +691,7 @@ int ddcca_conv_hist_hw(const float* in, int64_t n_maps, const ddcca_geom* gg, co
 }
 
 int ddcca_conv_hist_last_path(void) { return g_last_hist_path; }
+int ddcca_conv_last_path(void) { return g_last_conv_path; }
 
 int ddcca_conv_hist_dev(const float* in, int64_t n_maps, const ddcca_geom* gg, const float* conv_pack, int count,
                         int center, int block_h, int block_w, void* counts, int count_kind, int64_t groups_per_row,

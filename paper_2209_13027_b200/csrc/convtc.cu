@@ -92,8 +92,8 @@ __device__ __forceinline__ float pow2_scale(float mx) {
 // Two map values (scaled by sc) -> f16 pairs: hi = the scaled value truncated to 11 significant
 // bits (exact in f16 over its normal range), lo = rn_f16(value - hi) (the residual is exact in
 // float32); element 2 j in the low half of word j
-__device__ __forceinline__ void split2(float a, float b, float2 sc, uint32_t& hi, uint32_t& lo) {
-  const float2 v = __fmul2_rn(make_float2(a, b), sc);
+__device__ __forceinline__ void split2(float a, float b, float2 sc, float2 off, uint32_t& hi, uint32_t& lo) {
+  const float2 v = __ffma2_rn(make_float2(a, b), sc, off);  // (value - shift) * scale, one rounding
   const float2 h = make_float2(__uint_as_float(__float_as_uint(v.x) & 0xffffe000u),
                                __uint_as_float(__float_as_uint(v.y) & 0xffffe000u));
   const float2 r = __fadd2_rn(v, make_float2(-h.x, -h.y));
@@ -165,7 +165,8 @@ __device__ long long g_tc_trace[12][256];
 
 }  // namespace tc
 
-template <int L>
+// RESP: write the float32 responses (unscaled) instead of hashing them into block histograms
+template <int L, bool RESP>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     conv_hist_tc_kernel(TcHistArgs A, const float* __restrict__ taps /* [(dy * L + dx) * NF + f], zero mean */,
                         int nbuf /* staged map buffers: 2, or 1 when shared memory is short */,
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   const int nbins = 1 << A.nbits, words = (nbins + 1) / 2;
   const int nblk = A.nby * A.nbx;
-  const int cols = A.nbx * A.bw, rows = A.nby * A.bh;
+  const int cols = RESP ? A.q : A.nbx * A.bw, rows = RESP ? A.p : A.nby * A.bh;
   const int C = (cols + X - 1) / X;  // column blocks per map
   const int nch = 2 * C + 2;         // 4-column chunks staged per map (image columns -4 .. 8C + 3)
   uint8_t* bmat = smem;                                          // [L][hi, lo] banded B
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   // block; dfull / dempty: accumulators
   __shared__ uint64_t landed[2], ready[2], mapfree[2], full[NA], tfree[NA], dfull[2], dempty[2];
   __shared__ uint32_t tbase;
-  __shared__ float fscale[NF], lmax[2][LOAD_WARPS];
+  __shared__ float fscale[NF], lmax[2][LOAD_WARPS], lsum[2][LOAD_WARPS], mscale[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // per-filter power-of-two scales, then the banded B matrices (hi / lo), K-major core
@@ -205,7 +206,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     *reinterpret_cast<__half*>(bmat + (dy * 2 + hl) * BMAT_BYTES + (n >> 3) * 256 + (k >> 3) * 128 + (n & 7) * 16 +
                                (k & 7) * 2) = v;
   }
-  for (int w = tid; w < nblk * words; w += THREADS) bins[w] = 0u;
+  if constexpr (!RESP)
+    for (int w = tid; w < nblk * words; w += THREADS) bins[w] = 0u;
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&landed[i], 1);
@@ -257,27 +259,41 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           tma_load_3d(reinterpret_cast<float*>(dst + j * CHUNK_BYTES), &tmap, 4 * j - 4, -A.top, (int)m, &landed[bsel]);
       }
       mbar_wait_hw(&landed[bsel], use_par);
-      // largest magnitude: eight independent loads in flight per thread
-      float mx = 0.f;
+      // largest magnitude (and, with a DC shift, the sum): eight loads in flight per thread
+      float mx = 0.f, sm = 0.f;
       int e = lt;
       for (; e + 7 * 64 < n16; e += 8 * 64) {
         float4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const float4*>(dst + (e + 64 * u) * 16);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < 8; ++u) {
           mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+          if (RESP) sm += (v[u].x + v[u].y) + (v[u].z + v[u].w);
+        }
       }
       for (; e < n16; e += 64) {
         const float4 v = *reinterpret_cast<const float4*>(dst + e * 16);
         mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        if (RESP) sm += (v.x + v.y) + (v.z + v.w);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0) lmax[i & 1][warp - LOAD_WARP0] = mx;
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (RESP) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+      }
+      if (lane == 0) {
+        lmax[i & 1][warp - LOAD_WARP0] = mx;
+        lsum[i & 1][warp - LOAD_WARP0] = sm;
+      }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * LOAD_WARPS) : "memory");
-      const float sc = pow2_scale(fmaxf(lmax[i & 1][0], lmax[i & 1][1]));
-      const float2 sc2 = make_float2(sc, sc);
+      // DC shift (responses of centered windows: zero-mean taps make the result independent of
+      // a constant shift of the whole padded map, padding included): the map mean; the
+      // scale then bounds |v - shift| <= max |v| + |shift|
+      const float shift = (RESP && A.dc_shift) ? (lsum[i & 1][0] + lsum[i & 1][1]) / (float)(A.p * A.q) : 0.f;
+      const float sc = pow2_scale(fmaxf(lmax[i & 1][0], lmax[i & 1][1]) + fabsf(shift));
+      const float2 sc2 = make_float2(sc, sc), off2 = make_float2(-shift * sc, -shift * sc);
+      if (RESP && lt == 0) mscale[i & 7] = sc;  // read by the epilogue (at most ~5 blocks behind)
       e = lt;
       for (; e + 3 * 64 < n16; e += 4 * 64) {
         float4 v[4];
@@ -286,16 +302,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 o;
-          split2(v[u].x, v[u].y, sc2, o.x, o.z);
-          split2(v[u].z, v[u].w, sc2, o.y, o.w);
+          split2(v[u].x, v[u].y, sc2, off2, o.x, o.z);
+          split2(v[u].z, v[u].w, sc2, off2, o.y, o.w);
           *reinterpret_cast<uint4*>(dst + (e + 64 * u) * 16) = o;
         }
       }
       for (; e < n16; e += 64) {
         const float4 v = *reinterpret_cast<const float4*>(dst + e * 16);
         uint4 o;
-        split2(v.x, v.y, sc2, o.x, o.z);
-        split2(v.z, v.w, sc2, o.y, o.w);
+        split2(v.x, v.y, sc2, off2, o.x, o.z);
+        split2(v.z, v.w, sc2, off2, o.y, o.w);
         *reinterpret_cast<uint4*>(dst + e * 16) = o;
       }
       // generic-proxy writes that the next TMA into this buffer overwrites
@@ -433,6 +449,34 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (lane == 0) mbar_arrive(&dempty[grp]);
         if (q == 0) TC_TRACE(4, b0 + c);
         if (!row_ok) continue;
+        if constexpr (RESP) {
+          // responses: undo the power-of-two scales (exact) and store row y of the 8 columns of
+          // each filter (filter-minor output, cascade.py:123-125)
+          const float inv_m = 1.f / mscale[(uint32_t)((m - blockIdx.x) / gridDim.x) & 7];
+          const int x0 = X * c;
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            if (f >= A.count) break;
+            const float inv = inv_m / fscale[f];
+            float* o = A.resp + ((m * A.count + f) * (int64_t)A.p + y) * A.q + x0;
+            float r[X];
+#pragma unroll
+            for (int xo = 0; xo < X; ++xo) r[xo] = __uint_as_float(f < 4 ? v0[f * X + xo] : v1[(f - 4) * X + xo]) * inv;
+            if (x0 + X <= A.q && (A.q & 7) == 0) {
+              // one 256-bit store per (row, filter): a full 32-byte sector
+              asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(o), "f"(r[0]), "f"(r[1]),
+                           "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                           : "memory");
+            } else if (x0 + X <= A.q) {
+              reinterpret_cast<float4*>(o)[0] = make_float4(r[0], r[1], r[2], r[3]);
+              reinterpret_cast<float4*>(o)[1] = make_float4(r[4], r[5], r[6], r[7]);
+            } else {
+#pragma unroll
+              for (int xo = 0; xo < X; ++xo)
+                if (x0 + xo < A.q) o[xo] = r[xo];
+            }
+          }
+        } else {
         // sign bits -> LSB-first code; column n = f * X + xo: filters 0..3 in v0, 4..7 in v1.
         // Filters (2j, 2j + 1) are packed to bf16x2 (sign and zero preserved, no overflow; only
         // |r| < 1e-38 would flush, far below the float32 noise of responses scaled ~2^28) and
@@ -468,63 +512,66 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             }
           }
         }
+        }  // RESP / histogram epilogue
       }
-      // the map's histograms are complete: counts into the feature row, bins cleared
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-      if (warp == 0) TC_TRACE(7, (int)(2 * ((m - blockIdx.x) / gridDim.x)));
-      // The feature row holds the map's blocks' bins contiguously (encoder.py:71-99 layout), so
-      // the flush is a linear copy: bins (two 16-bit counts per word) -> u8 (saturated) or u16,
-      // 8 bins per thread step, the bins cleared behind it
-      {
-        const int64_t rowbase = (m / A.gpr) * A.row_stride + (m % A.gpr) * A.group_stride;
-        const int et = warp * 32 + lane;  // 0 .. 255
-        uint4* bins4 = reinterpret_cast<uint4*>(bins);
-        if ((nbins & 7) == 0) {
-          const int chunks = nblk * nbins / 8;
-          if (A.kind == 2) {
-            uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(A.counts) + rowbase);
-            for (int k = et; k < chunks; k += 32 * EPI_WARPS) {
-              o[k] = bins4[k];  // little-endian 16-bit halves are the u16 counts in bin order
-              bins4[k] = make_uint4(0u, 0u, 0u, 0u);
-            }
-          } else {
-            uint2* o = reinterpret_cast<uint2*>(static_cast<uint8_t*>(A.counts) + rowbase);
-            constexpr int U = 4, S = 32 * EPI_WARPS;  // four chunks in flight per thread
-            int k = et;
-            for (; k + (U - 1) * S < chunks; k += U * S) {
-              uint4 w[U];
-#pragma unroll
-              for (int u = 0; u < U; ++u) w[u] = bins4[k + u * S];
-#pragma unroll
-              for (int u = 0; u < U; ++u) {
-                const unsigned x = __vminu2(w[u].x, 0x00ff00ffu), y = __vminu2(w[u].y, 0x00ff00ffu);
-                const unsigned z = __vminu2(w[u].z, 0x00ff00ffu), v = __vminu2(w[u].w, 0x00ff00ffu);
-                o[k + u * S] = make_uint2(__byte_perm(x, y, 0x6420), __byte_perm(z, v, 0x6420));
-                bins4[k + u * S] = make_uint4(0u, 0u, 0u, 0u);
+      if constexpr (!RESP) {
+        // the map's histograms are complete: counts into the feature row, bins cleared
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (warp == 0) TC_TRACE(7, (int)(2 * ((m - blockIdx.x) / gridDim.x)));
+        // The feature row holds the map's blocks' bins contiguously (encoder.py:71-99 layout), so
+        // the flush is a linear copy: bins (two 16-bit counts per word) -> u8 (saturated) or u16,
+        // 8 bins per thread step, the bins cleared behind it
+        {
+          const int64_t rowbase = (m / A.gpr) * A.row_stride + (m % A.gpr) * A.group_stride;
+          const int et = warp * 32 + lane;  // 0 .. 255
+          uint4* bins4 = reinterpret_cast<uint4*>(bins);
+          if ((nbins & 7) == 0) {
+            const int chunks = nblk * nbins / 8;
+            if (A.kind == 2) {
+              uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(A.counts) + rowbase);
+              for (int k = et; k < chunks; k += 32 * EPI_WARPS) {
+                o[k] = bins4[k];  // little-endian 16-bit halves are the u16 counts in bin order
+                bins4[k] = make_uint4(0u, 0u, 0u, 0u);
+              }
+            } else {
+              uint2* o = reinterpret_cast<uint2*>(static_cast<uint8_t*>(A.counts) + rowbase);
+              constexpr int U = 4, S = 32 * EPI_WARPS;  // four chunks in flight per thread
+              int k = et;
+              for (; k + (U - 1) * S < chunks; k += U * S) {
+                uint4 w[U];
+  #pragma unroll
+                for (int u = 0; u < U; ++u) w[u] = bins4[k + u * S];
+  #pragma unroll
+                for (int u = 0; u < U; ++u) {
+                  const unsigned x = __vminu2(w[u].x, 0x00ff00ffu), y = __vminu2(w[u].y, 0x00ff00ffu);
+                  const unsigned z = __vminu2(w[u].z, 0x00ff00ffu), v = __vminu2(w[u].w, 0x00ff00ffu);
+                  o[k + u * S] = make_uint2(__byte_perm(x, y, 0x6420), __byte_perm(z, v, 0x6420));
+                  bins4[k + u * S] = make_uint4(0u, 0u, 0u, 0u);
+                }
+              }
+              for (; k < chunks; k += S) {
+                const uint4 w = bins4[k];
+                const unsigned x = __vminu2(w.x, 0x00ff00ffu), y = __vminu2(w.y, 0x00ff00ffu);
+                const unsigned z = __vminu2(w.z, 0x00ff00ffu), v = __vminu2(w.w, 0x00ff00ffu);
+                o[k] = make_uint2(__byte_perm(x, y, 0x6420), __byte_perm(z, v, 0x6420));
+                bins4[k] = make_uint4(0u, 0u, 0u, 0u);
               }
             }
-            for (; k < chunks; k += S) {
-              const uint4 w = bins4[k];
-              const unsigned x = __vminu2(w.x, 0x00ff00ffu), y = __vminu2(w.y, 0x00ff00ffu);
-              const unsigned z = __vminu2(w.z, 0x00ff00ffu), v = __vminu2(w.w, 0x00ff00ffu);
-              o[k] = make_uint2(__byte_perm(x, y, 0x6420), __byte_perm(z, v, 0x6420));
-              bins4[k] = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            for (int k = et; k < nblk * nbins; k += 32 * EPI_WARPS) {
+              const unsigned cnt = (bins[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
+              if (A.kind == 2)
+                static_cast<uint16_t*>(A.counts)[rowbase + k] = (uint16_t)cnt;
+              else
+                static_cast<uint8_t*>(A.counts)[rowbase + k] = (uint8_t)(cnt > 255u ? 255u : cnt);
             }
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+            for (int w = et; w < nblk * words; w += 32 * EPI_WARPS) bins[w] = 0u;
           }
-        } else {
-          for (int k = et; k < nblk * nbins; k += 32 * EPI_WARPS) {
-            const unsigned cnt = (bins[k >> 1] >> ((k & 1) * 16)) & 0xffffu;
-            if (A.kind == 2)
-              static_cast<uint16_t*>(A.counts)[rowbase + k] = (uint16_t)cnt;
-            else
-              static_cast<uint8_t*>(A.counts)[rowbase + k] = (uint8_t)(cnt > 255u ? 255u : cnt);
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-          for (int w = et; w < nblk * words; w += 32 * EPI_WARPS) bins[w] = 0u;
         }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
+        if (warp == 0) TC_TRACE(7, (int)(2 * ((m - blockIdx.x) / gridDim.x) + 1));
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory");
-      if (warp == 0) TC_TRACE(7, (int)(2 * ((m - blockIdx.x) / gridDim.x) + 1));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -534,21 +581,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 }
 
 template <int L>
-static size_t tc_smem(const TcHistArgs& a, int nbuf) {
+static size_t tc_smem(const TcHistArgs& a, int nbuf, bool resp) {
   using namespace tc;
-  const int C = (a.nbx * a.bw + X - 1) / X;
+  const int C = ((resp ? a.q : a.nbx * a.bw) + X - 1) / X;
   const int nbins = 1 << a.nbits;
   return (size_t)L * 2 * BMAT_BYTES + nbuf * (size_t)(2 * C + 2) * CHUNK_BYTES +
-         sizeof(unsigned) * (size_t)a.nby * a.nbx * ((nbins + 1) / 2);
+         (resp ? 0 : sizeof(unsigned) * (size_t)a.nby * a.nbx * ((nbins + 1) / 2));
 }
 constexpr size_t TC_SMEM_MAX = 225 * 1024;
 
-template <int L>
+template <int L, bool RESP>
 static int launch_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st) {
   using namespace tc;
   // two map buffers (the next map lands while this one is converted) when they fit
-  const int nbuf = tc_smem<L>(a, 2) <= TC_SMEM_MAX ? 2 : 1;
-  size_t smem = tc_smem<L>(a, nbuf);
+  const int nbuf = tc_smem<L>(a, 2, RESP) <= TC_SMEM_MAX ? 2 : 1;
+  size_t smem = tc_smem<L>(a, nbuf, RESP);
   if (smem > TC_SMEM_MAX) return DDCCA_ECONFIG;
   // one CTA per SM: it allocates all 512 TMEM columns (a second resident CTA would spin in
   // tcgen05.alloc until the first exits), so ask for more than half the shared memory
@@ -556,35 +603,55 @@ static int launch_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (!make_map(&tmap, a.in, a.n_maps, a.p, a.q, 4, RP, 1)) return DDCCA_ECONFIG;
-  auto kern = conv_hist_tc_kernel<L>;
+  auto kern = conv_hist_tc_kernel<L, RESP>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(a.n_maps, sms);
   kern<<<grid, THREADS, smem, st>>>(a, taps_dev, nbuf, tmap);
-  return check_launch("conv_hist_tc_kernel");
+  return check_launch(RESP ? "conv_resp_tc_kernel" : "conv_hist_tc_kernel");
+}
+
+static bool tc_shape_ok(const TcHistArgs& a) {
+  if (const char* e = getenv("DDCCA_CONV_TC"))
+    if (e[0] == '0') return false;  // A/B switch: FFMA kernels
+  // maps of <= 128 rows (one TMEM lane per row), <= 8 filters, odd windows up to 7 (the TMEM A
+  // ring of 3 x l x 16 columns plus 2 accumulators), TMA-aligned rows, "same" padding
+  if (a.p > 128 || a.count > tc::NF || a.n_maps < 1 || a.n_maps > INT32_MAX) return false;
+  if (a.q % 4 != 0 || (reinterpret_cast<uintptr_t>(a.in) & 15)) return false;
+  if (a.top != (a.l - 1) / 2 || a.left != (a.l - 1) / 2) return false;
+  return a.l == 3 || a.l == 5 || a.l == 7;
 }
 
 bool conv_hist_tc_covers(const TcHistArgs& a) {
-  if (const char* e = getenv("DDCCA_CONV_TC"))
-    if (e[0] == '0') return false;  // A/B switch: FFMA kernel
-  // maps of <= 128 rows (one TMEM lane per row), <= 8 filters / 8-bit codes, odd windows up
-  // to 7 (the TMEM A ring of 3 x l x 16 columns plus 2 accumulators), TMA-aligned rows
-  if (a.p > 128 || a.count > tc::NF || a.nbits > 8 || a.n_maps < 1 || a.n_maps > INT32_MAX) return false;
-  if (a.q % 4 != 0 || (reinterpret_cast<uintptr_t>(a.in) & 15)) return false;
-  if (a.top != (a.l - 1) / 2 || a.left != (a.l - 1) / 2) return false;
-  if (a.l != 3 && a.l != 5 && a.l != 7) return false;
+  if (!tc_shape_ok(a) || a.nbits > 8) return false;
   // a staged map, the banded B and the bins in shared memory
-  return tc_smem<7>(a, 1) <= TC_SMEM_MAX;
+  return tc_smem<7>(a, 1, false) <= TC_SMEM_MAX;
+}
+
+bool conv_resp_tc_covers(const TcHistArgs& a) {
+  // >= 2 column blocks per map (the epilogue's per-map scale ring assumes it), 32-byte stores
+  if (!tc_shape_ok(a) || a.q < 16 || (reinterpret_cast<uintptr_t>(a.resp) & 31)) return false;
+  return tc_smem<7>(a, 1, true) <= TC_SMEM_MAX;
 }
 
 int conv_hist_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st) {
   if (!conv_hist_tc_covers(a)) return DDCCA_ECONFIG;
   switch (a.l) {
-    case 3: return launch_tc<3>(a, taps_dev, st);
-    case 5: return launch_tc<5>(a, taps_dev, st);
-    case 7: return launch_tc<7>(a, taps_dev, st);
+    case 3: return launch_tc<3, false>(a, taps_dev, st);
+    case 5: return launch_tc<5, false>(a, taps_dev, st);
+    case 7: return launch_tc<7, false>(a, taps_dev, st);
+    default: return DDCCA_ECONFIG;
+  }
+}
+
+int conv_resp_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st) {
+  if (!conv_resp_tc_covers(a)) return DDCCA_ECONFIG;
+  switch (a.l) {
+    case 3: return launch_tc<3, true>(a, taps_dev, st);
+    case 5: return launch_tc<5, true>(a, taps_dev, st);
+    case 7: return launch_tc<7, true>(a, taps_dev, st);
     default: return DDCCA_ECONFIG;
   }
 }

@@ -14,6 +14,8 @@ struct TcHistArgs {
   int bh, bw, nby, nbx, kind, nbits;
   void* counts;
   int64_t gpr, row_stride, group_stride;
+  float* resp;   // responses mode: float32 output (n_maps * count, p, q), filter-minor
+  int dc_shift;  // responses mode: shift each map by its mean first (centered windows only)
 };
 
 constexpr int TC_FILTERS = 8;  // filter slots of the tensor-core kernel (zero-padded)
@@ -23,5 +25,8 @@ bool conv_hist_tc_covers(const TcHistArgs& a);
 // taps_dev: zero-mean taps [(dy * l + dx) * TC_FILTERS + f] in device memory (stream-ordered).
 // DDCCA_ECONFIG when the shape is not covered.
 int conv_hist_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st);
+// The same tensor-core convolution writing float32 responses ("same" padding, stride 1).
+bool conv_resp_tc_covers(const TcHistArgs& a);
+int conv_resp_tc(const TcHistArgs& a, const float* taps_dev, cudaStream_t st);
 
 }  // namespace ddcca

@@ -369,8 +369,17 @@ class Engine:
             fl = 2.0 * n * oh * ow * layer.count * layer.geom.dim
             by = 4.0 * n * (p * q + layer.count * oh * ow)
             dst = out.view(n, layer.count, oh, ow) if (out is not None and li == len(layers) - 1) else None
-            res = self._timed(f"conv_l{li + 1}", 1, {"kind": "fma", "flops": fl, "bytes": by}, conv, self.ex, cur,
+            name = f"conv_l{li + 1}"
+            res = self._timed(name, 1, {"kind": "fma", "flops": fl, "bytes": by}, conv, self.ex, cur,
                               layer, view, dst)
+            if self.profile is not None and _native.load().ddcca_conv_last_path() == 1:
+                # tcgen05 responses kernel (convtc.cu): HBM-bound (responses written back);
+                # executed tensor work as the conv-histogram's: 3 MMAs M128 N64 K16 per tap row
+                # and 8-column block, 128-row tiles
+                acc = self.work[name]
+                acc["kind"] = "hbm"
+                acc["tensor_flops"] = acc.get("tensor_flops", 0.0) + (
+                    2.0 * 128 * 64 * 16 * 3 * layer.geom.l1 * (-(-q // 8)) * (-(-p // 128)) * n)
             cur = res.view(n * layer.count, oh, ow)
         return cur
 

@@ -37,7 +37,7 @@ from make_golden import _import_reference  # noqa: E402
 from paper_2209_13027_b200 import synthetic  # noqa: E402  (numpy corpus generator only)
 
 OUT = Path(__file__).resolve().parent / "orl_accuracy.json"
-BATCHES = (128, 100, 96, 80, 64, 50, 40, 32)
+BATCHES = (128, 120, 112, 104, 100, 96, 90, 88, 80, 72, 64, 60, 56, 50, 48, 40, 36, 32, 25, 20)
 
 
 def main():

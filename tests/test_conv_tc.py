@@ -85,3 +85,40 @@ def test_tc_matches_ffma_and_oracle(ex, l, p, q, bh, monkeypatch):
     # every block keeps its pixel count
     per = tc.reshape(tc.shape[0], -1, plan.bins).sum(axis=2)
     assert (per == plan.bpc).all()
+
+
+@pytest.mark.parametrize("l,p,q,count,center,dc", [(7, 128, 128, 8, True, 0.0), (5, 64, 48, 8, True, 1000.0),
+                                                    (3, 100, 96, 6, False, 0.0), (7, 33, 40, 8, True, 5.0),
+                                                    (5, 128, 124, 4, True, 0.5)])
+def test_tc_responses_vs_ffma_and_oracle(ex, l, p, q, count, center, dc, monkeypatch):
+    """Responses mode (ddcca_conv on the tensor cores): float32-level agreement with the FFMA
+    kernel and the float64 oracle; centered windows shift each map by its mean first, so a large
+    DC offset (1000 + [0, 1)) costs no accuracy."""
+    rng = np.random.default_rng(l * 11 + q)
+    maps = (rng.uniform(size=(6, p, q)) + dc).astype(np.float32)
+    f = rng.standard_normal((count, l, l))
+    lib = _native.load()
+    dm = torch.from_numpy(maps).to(ex.device)
+    with torch.cuda.stream(ex.stream):
+        lay = E.layer_from_filters(ex, f, f, P.PatchGeometry(l, l), center)
+
+    def run(tc):
+        monkeypatch.setenv("DDCCA_CONV_TC", "1" if tc else "0")
+        with torch.cuda.stream(ex.stream):
+            out = E.conv(ex, dm, lay, 1)
+            path = lib.ddcca_conv_last_path()
+        ex.synchronize()
+        return out.cpu().numpy().astype(np.float64), path
+
+    got, path = run(True)
+    assert path == 1
+    ffma, path0 = run(False)
+    assert path0 == 0
+    ref = O.conv_stack(maps, O.Layer(f, f, O.Geometry(l, l), center), 1)
+    # the zero padding counts: shifted by the mean it is as far from it as the mean itself
+    mean = maps.mean(axis=(1, 2), keepdims=True)
+    spread = max(np.abs(maps - mean).max(), np.abs(mean).max()) if center else np.abs(maps).max()
+    scale = np.abs(f).sum(axis=(1, 2)).max() * spread
+    assert got.shape == ref.shape
+    assert np.abs(got - ref).max() <= 2e-6 * scale
+    assert np.abs(got - ffma).max() <= 4e-6 * scale

@@ -27,8 +27,10 @@ several points across its own batch decompositions on ORL):
   transform + oracle NN of the same (device-fitted) bank: within 0.5 pt;
 * device fit: its accuracy inside the reference's own band, widened by 0.5 pt.
 
-The device statistics differ from the oracle's only through the float32 maps of
-the lower layers (the lag products themselves are exact): ~1e-8 relative here.
+The device statistics differ from the oracle's through the float32 maps of the
+lower layers and, at layers >= 2 in the default blocked mode, the float32 lag
+products summed per TMA stage in float64 (layer-1 products are exact):
+~1e-8 - 1e-7 relative here.
 """
 
 import os

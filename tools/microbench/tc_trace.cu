@@ -13,6 +13,7 @@
 int main(int argc, char** argv) {
   using namespace ddcca;
   const int n = argc > 1 ? atoi(argv[1]) : 2048, p = 128, q = 128, l = 7;
+  const bool resp = argc > 2 && argv[2][0] == 'r';  // responses mode (ddcca_conv) instead of histograms
   std::vector<float> h((size_t)n * p * q), taps(l * l * TC_FILTERS);
   srand(1);
   for (auto& v : h) v = (float)rand() / RAND_MAX - 0.5f;
@@ -23,18 +24,22 @@ int main(int argc, char** argv) {
   cudaMalloc(&din, h.size() * 4);
   cudaMalloc(&dtaps, taps.size() * 4);
   cudaMalloc(&dcounts, (size_t)n * nby * nbx * 256);
+  float* dresp = nullptr;
+  if (resp) cudaMalloc(&dresp, (size_t)n * 8 * p * q * 4);
   cudaMemcpy(din, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dtaps, taps.data(), taps.size() * 4, cudaMemcpyHostToDevice);
   TcHistArgs a{};
   a.in = din; a.n_maps = n; a.p = p; a.q = q; a.top = 3; a.left = 3; a.l = l;
   a.count = 8; a.center = 1; a.bh = 16; a.bw = 16; a.nby = nby; a.nbx = nbx; a.kind = 0; a.nbits = 8;
   a.counts = dcounts; a.gpr = 1; a.row_stride = (int64_t)nby * nbx * 256; a.group_stride = 0;
-  for (int it = 0; it < 2; ++it) printf("rc %d\n", conv_hist_tc(a, dtaps, 0));
+  a.resp = dresp; a.dc_shift = 1;
+  auto launch = [&]() { return resp ? conv_resp_tc(a, dtaps, 0) : conv_hist_tc(a, dtaps, 0); };
+  for (int it = 0; it < 2; ++it) printf("rc %d\n", launch());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  conv_hist_tc(a, dtaps, 0);
+  launch();
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
