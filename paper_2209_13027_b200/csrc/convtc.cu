@@ -349,7 +349,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             dst[d][1] = make_uint4(c0.z, c0.w, c1.z, c1.w);
           }
       };
-      auto block = [&](const uint4 (&lf)[HALF][2], const uint4 (&rt)[HALF][2]) {
+      // block(lf, rt, next): stores block c from slots c (lf) and c + 1 (rt), and loads slot
+      // `next` into lf while the stores drain (lf's words are consumed by the stores' issue)
+      auto block = [&](uint4 (&lf)[HALF][2], const uint4 (&rt)[HALF][2], int next) {
         const uint32_t ia = blk % NA;
         if (blk >= NA) mbar_wait_hw(&tfree[ia], ((blk / NA) - 1) & 1);
         if (warp == PROD_WARP0) TC_TRACE(5, blk);
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
           st8(ta + col, hv);
           st8(ta + col + 8, lv);
         }
+        if (next <= C) load_slot(next, lf);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -374,13 +377,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         ++blk;
       };
       load_slot(0, sa);
+      load_slot(1, sb);
       for (int c = 0; c < C; c += 2) {
-        load_slot(c + 1, sb);
-        block(sa, sb);
-        if (c + 1 < C) {
-          load_slot(c + 2, sa);
-          block(sb, sa);
-        }
+        block(sa, sb, c + 2);      // block c = slots c, c + 1; sa <- slot c + 2
+        if (c + 1 < C) block(sb, sa, c + 3);  // block c + 1 = slots c + 1, c + 2; sb <- slot c + 3
       }
       // the map buffer is free once all producer warps are past it
       __syncwarp();
