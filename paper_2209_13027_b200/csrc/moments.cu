@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
     const unsigned bytes = (unsigned)stage_elems * 4u;
     for (int s = 0; s < nstages; ++s) {
       const int slot = s % NS;
-      if (s >= NS) mbar_wait_sleep(&empty[slot], (unsigned)((s / NS - 1) & 1), 200);
+      if (s >= NS) mbar_wait(&empty[slot], (unsigned)((s / NS - 1) & 1));
       if (lane == 0) {
         mbar_expect_tx(&full[slot], bytes);
         tma_load_3d(stage_mem + slot * max_stage, &tmap, x, y, (int)(ma + (int64_t)s * mb), &full[slot]);

@@ -54,15 +54,16 @@ def full(rep):
     txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     h = rows[0]
+    units = dict(zip(h, rows[1])) if len(rows) > 1 else {}  # second row: the metric units
     out = []
     for r in rows[2:]:
         d = dict(zip(h, r))
         out.append(f"**{d.get('Kernel Name', '?')}** (grid {d.get('launch__grid_size')}, block "
                    f"{d.get('launch__block_size')}, {d.get('launch__registers_per_thread')} regs)\n")
-        out.append("| metric | value |\n|---|---|")
+        out.append("| metric | value | unit |\n|---|---|---|")
         for k in KEYS[:1] + KEYS[1:]:
             if k in d and k not in ("launch__grid_size", "launch__block_size", "launch__registers_per_thread"):
-                out.append(f"| `{k}` | {d[k]} |")
+                out.append(f"| `{k}` | {d[k]} | {units.get(k, '')} |")
         stalls = []
         for k in h:
             if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):

@@ -25,7 +25,10 @@ def main(src, dst, label, workload="caltech256"):
     for r in rows[hi + 1:]:
         if len(r) < len(h):
             continue
-        name = r[ki].split("(")[0].replace("void ", "").replace("ddcca::", "").split("<")[0]
+        raw = r[ki].split("(")[0].replace("void ", "").replace("ddcca::", "")
+        name = raw.split("<")[0]
+        if name == "conv_hist_tc_kernel" and ("true" in raw or raw.endswith(", 1>")):
+            name = "conv_resp_tc_kernel"  # the responses mode of the tensor-core conv (hidden layers)
         agg[name][r[mi]] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         ids[name].add(r[idi])
     out = {"source": label, "workload": workload, "kernels": {}}
