@@ -1381,7 +1381,12 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
       bx.rows_short = g.l1;
       for (const Task& t : P.tasks)
         if (t.y1 - t.y0 < g.l1) bx.rows_short = std::max(bx.rows_short, t.y1 - t.y0 + g.l1 - 1);
-      bx.mb_short = std::max(1, std::min(8, stage_rows / bx.rows_short));
+      // short tasks (single border rows) do little work per map: the blocked form (float32
+      // stages, no float64 tiles) takes 16 maps per stage (-2 % layer-2 moments); the exact
+      // form keeps 8 (its float64 tiles would cost occupancy)
+      const bool blocked = (flags & DDCCA_MOMENTS_F32_BLOCKS) != 0;
+      bx.mb_short = blocked ? std::max(1, std::min(16, (stage_rows + 16) / bx.rows_short))
+                            : std::max(1, std::min(8, stage_rows / bx.rows_short));
       const int x_first = g.left - (g.l2 - 1) - g.left;  // tile origin column of the first column tile
       bx.shift = ((x_first % 4) + 4) % 4;
       const int tcb = (tcv + bx.shift + 3) / 4 * 4;

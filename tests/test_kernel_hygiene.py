@@ -118,8 +118,11 @@ def test_conv_hist_repeatable_and_in_bounds(ex, l, count, p, q, bh, bw, tc, monk
     assert E.decode_counts(outs[0], plan).reshape(40, -1, plan.bins).sum(axis=2).min() == plan.bpc
 
 
-@pytest.mark.parametrize("l,count,p,q", [(7, 8, 40, 36), (5, 8, 23, 30), (9, 12, 33, 41), (3, 8, 5, 6)])
+@pytest.mark.parametrize("l,count,p,q", [(7, 8, 40, 36), (5, 8, 23, 30), (9, 12, 33, 41), (3, 8, 5, 6),
+                                         (7, 8, 128, 128), (5, 6, 100, 92)])
 def test_conv_repeatable_and_in_bounds(ex, l, count, p, q):
+    """Hidden-layer convs: the tensor-core responses kernel where covered ((7, 8, 40, 36),
+    (7, 8, 128, 128), (5, 6, 100, 92)), the FFMA kernels otherwise."""
     rng = np.random.default_rng(l * 3 + q)
     maps = torch.from_numpy(_maps(rng, 9, p, q)).to(ex.device)
     f = rng.standard_normal((count, l, l))
