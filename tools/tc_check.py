@@ -1,4 +1,5 @@
-"""A/B of the fused conv-histogram: tcgen05 3xTF32 kernel (convtc.cu) vs the FFMA kernel vs the oracle.
+"""A/B of the fused conv-histogram: tcgen05 kind::f16 kernel (convtc.cu, scaled two-term split) vs the FFMA
+kernel vs the oracle.
 
 python tools/tc_check.py [n_maps] [l] [p] [q] [bh]
 """
