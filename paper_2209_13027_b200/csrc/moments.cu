@@ -531,8 +531,10 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 
 // One launch per (view, task kind): the single tensor map is used directly from
 // the parameter space (no runtime selection of a tensor-map address).
-template <int L1, int TCB>
-__global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
+// BLK: the blocked form only, its float64 sums in shared memory instead of registers (~60
+// registers: three CTAs per SM instead of two, more warps to cover the stage ring)
+template <int L1, int TCB, bool BLK>
+__global__ void __launch_bounds__(256, BLK ? 3 : (L1 <= 9 ? 2 : 1))
     lag_tma_kernel(LagArgs A, TmaBoxes bx, const int* __restrict__ task_ids, int view,
                    const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) float stage_mem[];
@@ -586,6 +588,57 @@ __global__ void __launch_bounds__(256, (L1 <= 9 ? 2 : 1))
       }
       __syncwarp();
     }
+  } else if constexpr (BLK) {
+    // ---------------- consumers, blocked form, float64 sums in shared memory ----------------
+    // accs[(dy * KDX + k) * cth + thread]: consecutive threads on consecutive words
+    double* accs = reinterpret_cast<double*>(empty + NS);
+    const int ct = threadIdx.x, cth = G * 32;
+#pragma unroll
+    for (int i = 0; i < L1 * KDX; ++i) accs[i * cth + ct] = 0.0;
+    const int cown = lane + (A.l2 - 1) + bx.shift;
+    const int cpart = lane + grp * KDX + bx.shift;
+    const bool skip0 = (grp * KDX + KDX - 1) < (A.l2 - 1);
+    const int kk = min(KDX, 2 * A.l2 - 1 - grp * KDX);
+    F32Partials<L1> fp;
+    f32_zero(fp);
+    for (int s = 0; s < nstages; ++s) {
+      const int slot = s % NS;
+      mbar_wait(&full[slot], (unsigned)((s / NS) & 1));
+      const float* tile = stage_mem + slot * max_stage;
+      const int64_t ms = ma + (int64_t)s * mb;
+      const int nm = (int)min((int64_t)mb, mbnd - ms);
+      for (int j = 0; j < nm; ++j)
+        lag_map_f32<L1, TCB>(tile + j * tile_elems, nrows, cown, cpart, short_task, skip0, kk, fp);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      // one float64 flush per stage (static lag indices on every branch)
+#pragma unroll
+      for (int dy = 0; dy < L1; ++dy) {
+        double* a0 = accs + (dy * KDX) * cth + ct;
+        if (kk >= 2) {
+          a0[0] += (double)fp.fa2[dy].x;
+          a0[cth] += (double)fp.fa2[dy].y;
+          if (kk >= 3) a0[2 * cth] += (double)fp.fa1[dy];
+        } else {
+          a0[0] += (double)fp.fa1[dy];
+        }
+      }
+      f32_zero(fp);
+    }
+    const int rslot = A.lane_slot[task * TILE_X + lane];
+    const int xg = T.x0 + lane;
+    const bool in_big = (rslot < 0) && (xg < A.xend);
+    double* out = A.rec + (((int64_t)batch * 2 + view) * A.nsplit + split) * (int64_t)A.nrec * A.NDF;
+    const int any_big = __any_sync(0xffffffffu, in_big);
+    for (int dy = 0; dy < L1; ++dy)
+      for (int k = 0; k < KDX; ++k) {
+        const int lag = dy * A.NDX + grp * KDX + k;
+        const double a = accs[(dy * KDX + k) * cth + ct];
+        double v = in_big ? a : 0.0;
+        v = warp_sum(v);
+        if (lane == 0 && any_big) out[(int64_t)T.rec0 * A.NDF + lag] = v;
+        if (rslot >= 0) out[(int64_t)(T.rec0 + rslot) * A.NDF + lag] = a;
+      }
   } else {
     // ---------------- consumers ----------------
     double acc[L1][KDX];
@@ -1406,8 +1459,11 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
         // float64 path: two compute tiles (one barrier per stage) and, by default, two float32
         // TMA stages, so two CTAs still fit one SM
         if (bx.f64 && !bx.f32blocks) bx.ns = std::max(2, std::min(8, env_int("DDCCA_TMA_STAGES", 2)));
+        // blocked form: float64 sums in shared memory, two stages (three CTAs per SM fit)
+        if (bx.f32blocks) bx.ns = std::max(2, std::min(8, env_int("DDCCA_TMA_STAGES", 2)));
         const size_t tsmem = sizeof(float) * bx.ns * max_stage + (2 * bx.ns + 1) * sizeof(uint64_t) +
-                             (bx.f64 ? 2 * sizeof(double) * max_stage : 0);
+                             (bx.f64 ? 2 * sizeof(double) * max_stage : 0) +
+                             (bx.f32blocks ? sizeof(double) * (size_t)P.G * 32 * g.l1 * KDX : 0);
         dim3 tblock(32 * (P.G + 1));
         // task ids by kind, uploaded after the plan tables
         std::vector<int> ids_int, ids_short;
@@ -1432,9 +1488,15 @@ int ddcca_moments_partial_ex(const float* maps1, const float* maps2, const int32
                   A, bx, ids_dev + ids_int.size(), v, tm[2 + v]);
           }
         };
-        if (g.l1 == 5 && tcb == 40) { tgo(lag_tma_kernel<5, 40>); launched = true; }
-        else if (g.l1 == 7 && tcb == 48) { tgo(lag_tma_kernel<7, 48>); launched = true; }
-        else if (g.l1 == 9 && tcb == 52) { tgo(lag_tma_kernel<9, 52>); launched = true; }
+        if (bx.f32blocks) {
+          if (g.l1 == 5 && tcb == 40) { tgo(lag_tma_kernel<5, 40, true>); launched = true; }
+          else if (g.l1 == 7 && tcb == 48) { tgo(lag_tma_kernel<7, 48, true>); launched = true; }
+          else if (g.l1 == 9 && tcb == 52) { tgo(lag_tma_kernel<9, 52, true>); launched = true; }
+        } else {
+          if (g.l1 == 5 && tcb == 40) { tgo(lag_tma_kernel<5, 40, false>); launched = true; }
+          else if (g.l1 == 7 && tcb == 48) { tgo(lag_tma_kernel<7, 48, false>); launched = true; }
+          else if (g.l1 == 9 && tcb == 52) { tgo(lag_tma_kernel<9, 52, false>); launched = true; }
+        }
       }
     }
     if (launched) {
