@@ -514,9 +514,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for r in ([roof] if roof is not None else []) + list(rooflines.values()):
         name = r["kernel"]
         conv_k = "conv_resp_tc_kernel" if r.get("bound") == "hbm" else "conv_c_kernel"
+        lag_k = "lag_tma_blk_kernel" if r.get("bound") == "fp32_fma" else "lag_tma_kernel"
         kname = {"conv_hist": "conv_hist_tc_kernel" if r.get("bound") == "tensor" else "conv_hist_kernel",
-                 "conv_l1": conv_k, "conv_l2": conv_k}.get(
-            name, "lag_tma_kernel" if name.startswith("moments") else name)
+                 "conv_l1": conv_k, "conv_l2": conv_k}.get(name, lag_k if name.startswith("moments") else name)
         k = tfd.get("kernels", {}).get(kname) if tfd.get("workload", "caltech256") == args.workload else None
         if k:
             r["traffic"] = k["dram_bytes_per_launch"]

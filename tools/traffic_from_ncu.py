@@ -29,6 +29,8 @@ def main(src, dst, label, workload="caltech256"):
         name = raw.split("<")[0]
         if name == "conv_hist_tc_kernel" and ("true" in raw or raw.endswith(", 1>")):
             name = "conv_resp_tc_kernel"  # the responses mode of the tensor-core conv (hidden layers)
+        if name == "lag_tma_kernel" and ("true" in raw or raw.endswith(", 1>")):
+            name = "lag_tma_blk_kernel"  # the blocked (float32-product) instantiation
         agg[name][r[mi]] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
         ids[name].add(r[idi])
     out = {"source": label, "workload": workload, "kernels": {}}
