@@ -35,6 +35,7 @@ MAP_BUDGET_BYTES = 6 << 30  # per view, per super-batch (deepest layer input)
 KEEP_MAPS_BYTES = 48 << 30  # fit keeps the last layer's input maps (both views) for the transform if they fit
 MOMENTS_F32_BLOCKS = 1  # ddcca.h DDCCA_MOMENTS_F32_BLOCKS
 MOMENTS_FINE_SPLITS = 2  # ddcca.h DDCCA_MOMENTS_FINE_SPLITS
+FINE_ALL_MAPS = 8192  # fits with fewer maps per view at a layer use 32-map splits there too
 HOST_CHUNK_BATCHES = 4  # sample batches per streamed device->host count copy
 
 
@@ -325,6 +326,7 @@ class Engine:
         self.ex = executor
         self.budget = map_budget_bytes
         self.uploader = None  # cascade.ChunkedUpload of an in-flight chunked image upload
+        self.n_global_fit = None  # global sample count of the fit in progress (moments_flags)
         self.keep_maps_bytes = keep_maps_bytes
         self.maps_cache = None  # last hidden layer's maps of the fitted shard, reused by the transform
         self.profile = None   # dict name -> [(start_event, end_event)] when profiling
@@ -492,10 +494,16 @@ class Engine:
         return parts
 
     def moments_flags(self, layers: list) -> int:
-        """Float32-blocked lag products for layers fed by filter responses (ExecSettings.moments)."""
+        """Float32-blocked lag products for layers fed by filter responses (ExecSettings.moments);
+        32-map splits (4x the CTAs) for the first layer (one map per sample) and for every layer
+        of a small fit (fewer than FINE_ALL_MAPS maps per view at the layer, all ranks together:
+        their lag grids would not fill the GPU). Both depend only on the layer and the global
+        sample count, never on how batches are grouped into calls or ranks, so the partials stay
+        bitwise independent of the GPU count."""
         mode = getattr(self.ex.settings, "moments", "blocked")
         flags = MOMENTS_F32_BLOCKS if (layers and mode == "blocked") else 0
-        if not layers:  # one map per sample: 32-map splits (4x the CTAs of the first layer)
+        n = self.n_global_fit
+        if not layers or (n is not None and n * self._maps_per_sample(layers) < FINE_ALL_MAPS):
             flags |= MOMENTS_FINE_SPLITS
         return flags
 
@@ -531,6 +539,7 @@ class Engine:
         ex = self.ex
         m_local = images1.shape[0]
         n_global = m_local if n_global is None else n_global
+        self.n_global_fit = n_global  # fixes the split policy of every layer (moments_flags)
         gb = [range(s, min(s + batch_size, n_global)) for s in range(0, n_global, batch_size)]
         mine = ex.shard(len(gb))
         local = [gb[b] for b in mine]
